@@ -1,0 +1,149 @@
+/*
+ * randutv.h -- C ABI of the B200-native randUTV hot path.
+ *
+ * randUTV (Martinsson, Quintana-Ortí, Heavner, arXiv 1703.00998) factors a
+ * dense fp64 m x n matrix as  A = U T V^T  with U, V orthogonal and T upper
+ * triangular (Eq. eq:defUTVpre), one block of b columns per
+ * step, following the efficient algorithm of Fig. fig:randUTV
+ * (PAPER.md:919-989).  Every step of the computation runs in the library's
+ * own sm_100a CUDA kernels.
+ *
+ * Conventions shared by every entry point
+ *   - Matrices are fp64 (double), COLUMN-MAJOR: element (i, j) of a matrix
+ *     with leading dimension ld is p[i + j*ld].
+ *   - Pointers may be CUDA device pointers or host pointers, as stated per
+ *     function.  The caller owns every buffer; the library never frees them.
+ *   - ``stream`` arguments are cudaStream_t values passed as void*; NULL means
+ *     cudaStreamPerThread.  Functions returning after completion say so.
+ *   - Return value (LAPACK ``info`` style): 0 = success; -k = argument k
+ *     (1-based, in the order of randutv_factor's parameter list) is invalid;
+ *     RANDUTV_ERR_* (> 0) below otherwise.  randutv_strerror() names them.
+ *   - The library keeps one cached device workspace per process (grown on
+ *     demand, guarded by a mutex); calls from several host threads serialise.
+ */
+#ifndef RANDUTV_H
+#define RANDUTV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RANDUTV_API __attribute__((visibility("default")))
+#else
+#define RANDUTV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RANDUTV_OK 0
+#define RANDUTV_ERR_NONFINITE 1   /* A holds NaN or Inf                */
+#define RANDUTV_ERR_CUDA 2        /* a CUDA runtime error                             */
+#define RANDUTV_ERR_NOMEM 3       /* device allocation failed                         */
+#define RANDUTV_ERR_NCCL 4        /* reserved for the multi-GPU path                  */
+#define RANDUTV_ERR_UNSUPPORTED 5 /* shape outside this build (e.g. > 65536 rows)    */
+
+#define RANDUTV_MAX_B 1024
+
+/* Options of randutv_factor_ex.  Zero-initialise, then set what you need. */
+typedef struct randutv_opts {
+  void* stream;           /* cudaStream_t to enqueue on (NULL: per-thread stream)          */
+  double tol;             /* > 0: stop after a step once ||T(I3,J3)||_F <= tol ||A||_F       */
+  int32_t no_reortho;     /* 0 (default): re-orthonormalise Y before every X Y in the power
+                             loop (R5); 1: plain power loop      */
+  int32_t reserved0;
+  void* workspace;        /* optional caller device workspace (NULL: library cache)        */
+  size_t workspace_bytes; /* its size; must be >= randutv_workspace_size(...)              */
+} randutv_opts;
+
+/* Diagnostics filled by randutv_factor_ex (may be NULL). */
+typedef struct randutv_info {
+  int64_t k_done;       /* columns processed: n for a full factorisation                 */
+  int32_t steps;        /* randomised steps taken (the ``if`` branch of P:939)           */
+  int32_t final_block;  /* 1 if the final SVD block (``else`` branch) ran         */
+  int32_t max_sweeps;   /* most Jacobi sweeps any small SVD needed                       */
+  int32_t reserved0;
+  double trailing_fro;  /* ||T(k_done+1:m, k_done+1:n)||_F (0 for a full factorisation)  */
+  double a_fro;         /* ||A||_F                                                        */
+} randutv_info;
+
+/*
+ * randutv_factor -- A = U T V^T  (Fig. fig:randUTV).
+ *
+ *  1 m, 2 n    sizes, 1 <= n <= m (the fat case m < n, is not
+ *              built: returns -2)
+ *  3 A         m x n input, leading dimension 4 lda >= m.  Read only.  Host or
+ *              device memory.  May alias T when lda == m (in-place).
+ *  5 b         block size, 1 <= b <= RANDUTV_MAX_B
+ *  6 q         power-iteration steps, q >= 0
+ *  7 seed      Philox key of the Gaussian sketches G (R2)
+ *  8 k_stop    0 = full factorisation; > 0 = stop before the first step whose
+ *              offset b(i-1) >= k_stop (so k_done = b*ceil(k_stop/b))
+ *  9 U         m x m output (ld = m) or NULL
+ * 10 T         m x n output (ld = m), required.  On return T is upper
+ *              triangular with exact zeros below the diagonal over the
+ *              processed columns; each processed b x b diagonal block is
+ *              diagonal, non-negative and non-increasing.
+ * 11 V         n x n output (ld = n) or NULL.  U and V must both be given or
+ *              both be NULL; NULL selects the paper's "no orthonormal
+ *              matrices" mode.
+ * U, T, V must all be host or all be device memory.  Host buffers are staged
+ * through device memory inside the call.  Returns after completion.
+ */
+RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, uint64_t seed,
+                   int64_t k_stop, double* U, double* T, double* V);
+
+/* As randutv_factor, with options and diagnostics.  Device pointers are
+ * processed asynchronously on opts->stream, except that the call synchronises
+ * that stream once after validating A (non-finite scan) and once per step when
+ * opts->tol > 0 (early-stop test).  Returns after all work is enqueued; with
+ * host buffers it returns after completion. */
+RANDUTV_API int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
+                      int32_t q, uint64_t seed, int64_t k_stop, double* U, double* T, double* V,
+                      randutv_info* info);
+
+/* Device workspace bytes randutv_factor_ex needs for this shape
+ * (with_uv != 0: U and V requested). */
+RANDUTV_API size_t randutv_workspace_size(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv);
+
+RANDUTV_API const char* randutv_strerror(int code);
+RANDUTV_API const char* randutv_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Component entry points (device pointers only, asynchronous on ``stream``).
+ * They expose the kernels the factorisation is built from so that each can be
+ * checked against the oracle on the same bytes.
+ * ------------------------------------------------------------------------ */
+
+/* G (rows x cols, ld ldg) = the step's Gaussian test matrix, PAPER.md:941:
+ * Philox4x32-10 with key (lo32 seed, hi32 seed), counter (row/2, col, step,
+ * purpose), Box-Muller (R2). */
+RANDUTV_API int randutv_gaussian(double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed, uint32_t step,
+                     uint32_t purpose, void* stream);
+
+/* C = alpha op(A) op(B) + beta C on the FP64 tensor cores (DMMA).
+ * transa/transb: 0 = N, 1 = T.  op(A) is M x K, op(B) K x N, C M x N. */
+RANDUTV_API int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* Unpivoted Householder QR of the m x b panel in V (ld ldv, m >= b), in place
+ * (dlarfg sign convention, R3).  On return V holds
+ * the explicit unit-lower-trapezoidal reflectors, R (b x b, ld ldr) the upper
+ * triangular factor with zeros below, tau[b] the scalars and Tw (b x b, ld
+ * ldt) the forward compact-WY factor: H_1...H_b = I - V Tw V^T. */
+RANDUTV_API int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                     double* Tw, int64_t ldt, void* stream);
+
+/* Batched SVD of ``batch`` k x k matrices: R_i at R + i*strideR
+ * (ld ldr) = Us_i diag(D_i) Vs_i^T, D_i >= 0 non-increasing.  D is batch x k,
+ * Us and Vs are batch consecutive k x k blocks (ld k).  sweeps (may be NULL)
+ * receives the Jacobi sweep count per matrix. */
+RANDUTV_API int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,
+                              double* Us, double* Vs, int32_t* sweeps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANDUTV_H */

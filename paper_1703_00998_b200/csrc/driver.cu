@@ -1,0 +1,573 @@
+// Host driver of the blocked randUTV (Fig. fig:randUTV) and
+// the C ABI of include/randutv.h.  The driver only enqueues kernels; every
+// arithmetic step runs on the GPU.
+//
+// Per randomized step i (offset r0 = b(i-1), X = T(r0:m, r0:n)):
+//   G = Philox Gaussian (m_i x b)
+//   Y = X^T G;  q x { [Y <- thinQ(Y)]; Z = X Y; Y = X^T Z }        P:942-945 (+R5)
+//   (W_v, T_v) = householder(Y)
+//   T(:, r0:n) -= ((T(:, r0:n) W_v) T_v) W_v^T   (all m rows)     P:950 (R6)
+//   (W_u, T_u, R11) = householder(T(r0:m, J2))
+//   C = T(r0:m, J3):  C -= W_u ((C^T W_u) T_u)^T
+//   T(I2, J2) = R11, T(I3, J2) = 0
+// The b x b SVDs and their folds act only on rows I2 / columns J2,
+// which later steps never touch, and left/right multiplications commute, so
+// they are deferred and batched after the loop (SURVEY §0 finding 3,
+// DESIGN.md R13).  U and V are formed, when requested, by backward
+// accumulation of the stored reflectors: U = U_1...U_s blockdiag(Us_i).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/randutv.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace rutv;
+
+namespace {
+
+std::mutex g_mu;
+void* g_ws = nullptr;
+size_t g_ws_bytes = 0;
+
+struct Plan {
+  int64_t m, n, b;
+  int q;
+  bool uv;
+  int64_t s;          // loop bound min(ceil(m/b), ceil(n/b))
+  int64_t nrand;      // number of randomized steps possible
+  // offsets (doubles) of per-step reflector slots when uv
+  std::vector<size_t> off_v, off_u;
+  size_t elems_v = 0, elems_u = 0;
+};
+
+Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv) {
+  Plan p;
+  p.m = m; p.n = n; p.b = b; p.q = q; p.uv = uv;
+  p.s = std::min(cdiv(m, b), cdiv(n, b));
+  p.nrand = 0;
+  for (int64_t i = 1; i <= p.s; ++i)
+    if (b * i < m && b * i < n) p.nrand = i;
+  if (uv) {
+    for (int64_t i = 1; i <= p.s; ++i) {
+      int64_t r0 = b * (i - 1);
+      p.off_v.push_back(p.elems_v);
+      p.off_u.push_back(p.elems_u);
+      p.elems_v += size_t(n - r0) * b;
+      p.elems_u += size_t(m - r0) * b;
+    }
+  }
+  return p;
+}
+
+struct Work {
+  double *G, *Y, *Y2, *P, *P2, *Vu, *Wt, *Wt2, *tau, *Rtmp, *Ttmp;
+  double *Tv, *Tu, *Rall, *Dall, *Usall, *Vsall, *jwork;
+  double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf;
+  double *Wv_all, *Wu_all;
+  double *fold, *part, *nrm, *scal;
+  int* flag;
+  int* sweeps;
+  size_t part_elems;
+  QrWork qw;
+};
+
+Work carve(Arena& ar, const Plan& p) {
+  Work w{};
+  const int64_t m = p.m, n = p.n, b = p.b, mx = std::max(m, n);
+  const int64_t sb = std::max<int64_t>(p.nrand, 1);
+  w.G = ar.take<double>(size_t(m) * b);
+  w.Y = ar.take<double>(size_t(n) * b);
+  w.Y2 = ar.take<double>(size_t(n) * b);
+  w.P = ar.take<double>(size_t(m) * b);
+  w.P2 = ar.take<double>(size_t(m) * b);
+  w.Vu = ar.take<double>(size_t(m) * b);
+  w.Wt = ar.take<double>(size_t(n) * b);
+  w.Wt2 = ar.take<double>(size_t(n) * b);
+  w.tau = ar.take<double>(size_t(b));
+  w.Rtmp = ar.take<double>(size_t(b) * b);
+  w.Ttmp = ar.take<double>(size_t(b) * b);
+  w.Tv = ar.take<double>(size_t(sb) * b * b);
+  w.Tu = ar.take<double>(size_t(sb + 1) * b * b);
+  w.Rall = ar.take<double>(size_t(sb) * b * b);
+  w.Dall = ar.take<double>(size_t(sb) * b);
+  w.Usall = ar.take<double>(size_t(sb) * b * b);
+  w.Vsall = ar.take<double>(size_t(sb) * b * b);
+  w.jwork = ar.take<double>(jacobi_work_elems((int)sb, (int)b));
+  w.Rfin = ar.take<double>(size_t(b) * b);
+  w.Dfin = ar.take<double>(size_t(b));
+  w.Usfin = ar.take<double>(size_t(b) * b);
+  w.Vsfin = ar.take<double>(size_t(b) * b);
+  w.jworkf = ar.take<double>(jacobi_work_elems(1, (int)b));
+  if (p.uv) {
+    w.Wv_all = ar.take<double>(p.elems_v);
+    w.Wu_all = ar.take<double>(p.elems_u);
+  }
+  w.fold = ar.take<double>(size_t(mx) * b);
+  w.part_elems = size_t(8) * mx * b + size_t(148) * 32 * 1024;
+  w.part = ar.take<double>(w.part_elems);
+  w.qw.part = w.part;
+  w.qw.part_elems = w.part_elems;
+  w.qw.sfull = ar.take<double>(size_t(32) * b);
+  w.qw.s2 = ar.take<double>(size_t(32) * b);
+  w.qw.z = ar.take<double>(size_t(32) * b);
+  w.nrm = ar.take<double>(8192);
+  w.scal = ar.take<double>(16);
+  w.flag = ar.take<int>(16);
+  w.sweeps = ar.take<int>(size_t(sb) + 16);
+  return w;
+}
+
+size_t workspace_bytes(const Plan& p) {
+  Arena ar;
+  ar.dry = true;
+  carve(ar, p);
+  return ar.off + 4096;
+}
+
+enum MemKind { MEM_DEVICE, MEM_HOST };
+
+MemKind mem_kind(const void* ptr) {
+  if (!ptr) return MEM_DEVICE;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return MEM_HOST;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? MEM_DEVICE : MEM_HOST;
+}
+
+void dg(const Work& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+        const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems);
+}
+
+int check_qr(int rc) {
+  if (rc != OK) throw rc;
+  return rc;
+}
+
+// The factorization proper (device pointers only).
+int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
+                  uint64_t seed, int64_t k_stop, double* U, double* T, double* V, randutv_info* info,
+                  void* ws, size_t ws_bytes) {
+  cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+  const bool uv = (U != nullptr);
+  const bool reortho = (o.no_reortho == 0);
+  Plan p = make_plan(m, n, b, q, uv);
+  Arena ar;
+  ar.base = (char*)ws;
+  ar.size = ws_bytes;
+  Work w = carve(ar, p);
+
+  // ---- T <- A, ||A||_F, non-finite scan (one host sync)
+  RUTV_CK(cudaMemsetAsync(w.flag, 0, sizeof(int), st));
+  copy_norm_check(st, m, n, A, lda, T, m, w.nrm, w.scal, w.flag);
+  double a2 = 0.0;
+  int bad = 0;
+  RUTV_CK(cudaMemcpyAsync(&a2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+  RUTV_CK(cudaMemcpyAsync(&bad, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RUTV_CK(cudaStreamSynchronize(st));
+  if (bad) return RANDUTV_ERR_NONFINITE;
+  const double a_fro = std::sqrt(a2);
+
+  int64_t steps = 0, k_done = 0;
+  bool final_block = false, final_tall = false;
+  int64_t r0f = 0, nif = 0, mif = 0;
+  double trailing = 0.0;
+  bool stopped = false;
+
+  for (int64_t i = 1; i <= p.s; ++i) {
+    const int64_t r0 = b * (i - 1);
+    if (k_stop > 0 && r0 >= k_stop) { stopped = true; break; }
+    const int64_t e2 = std::min(b * i, m), f2 = std::min(b * i, n);
+    const int64_t mi = m - r0, ni = n - r0;
+    double* X = T + r0 + r0 * m;
+    if (b * i < m && b * i < n) {
+      const int64_t si = i - 1;  // 0-based step slot
+      // ---- sketch
+      gaussian_fill(st, w.G, m, mi, b, seed, uint32_t(i - 1), 0u);
+      dg(w, st, true, false, ni, b, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
+      double* Ycur = w.Y;
+      double* Yalt = w.Y2;
+      for (int it = 0; it < q; ++it) {
+        if (reortho) {
+          check_qr(panel_qr(st, ni, b, Ycur, n, w.Rtmp, b, w.tau, w.Ttmp, b, w.qw));
+          thin_q(st, ni, b, Ycur, n, w.Ttmp, b, Yalt, n, w.Rtmp, w.part, w.part_elems);
+          std::swap(Ycur, Yalt);
+        }
+        dg(w, st, false, false, mi, b, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);       // Z = X Y
+        dg(w, st, true, false, ni, b, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);        // Y = X^T Z
+      }
+      // ---- V block: Householder QR of Y
+      double* Wv = Ycur;
+      int64_t ldwv = n;
+      if (uv) {
+        Wv = w.Wv_all + p.off_v[si];
+        ldwv = ni;
+        copy_matrix(st, ni, b, Ycur, n, Wv, ldwv);
+      }
+      double* Tv = w.Tv + size_t(si) * b * b;
+      check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, w.qw));
+      // ---- right apply to all m rows
+      double* TJ = T + r0 * m;
+      dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
+      dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
+      dg(w, st, false, true, m, ni, b, -1.0, w.P2, m, Wv, ldwv, 1.0, TJ, m);
+      // ---- U block: Householder QR of the panel T(r0:m, J2)
+      double* Wu = w.Vu;
+      int64_t ldwu = m;
+      if (uv) {
+        Wu = w.Wu_all + p.off_u[si];
+        ldwu = mi;
+      }
+      copy_matrix(st, mi, b, X, m, Wu, ldwu);
+      double* Tu = w.Tu + size_t(si) * b * b;
+      double* R11 = w.Rall + size_t(si) * b * b;
+      check_qr(panel_qr(st, mi, b, Wu, ldwu, R11, b, w.tau, Tu, b, w.qw));
+      // T(I2,J2) = R11 (replaced by D after the batched SVD), T(I3,J2) = 0
+      copy_matrix(st, b, b, R11, b, X, m);
+      set_zero(st, mi - b, b, X + b, m);
+      // ---- left apply to T(r0:m, J3)
+      const int64_t nc = n - f2;
+      double* Cm = T + r0 + f2 * m;
+      dg(w, st, true, false, nc, b, mi, 1.0, Cm, m, Wu, ldwu, 0.0, w.Wt, n);       // C^T W_u
+      dg(w, st, false, false, nc, b, b, 1.0, w.Wt, n, Tu, b, 0.0, w.Wt2, n);        // (C^T W_u) T_u
+      dg(w, st, false, true, mi, nc, b, -1.0, Wu, ldwu, w.Wt2, n, 1.0, Cm, m);      // C -= W_u (.)^T
+      ++steps;
+      k_done = f2;
+      if (o.tol > 0.0) {
+        double t2 = 0.0;
+        fro2(st, m - e2, n - f2, T + e2 + f2 * m, m, w.nrm, w.scal);
+        RUTV_CK(cudaMemcpyAsync(&t2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+        RUTV_CK(cudaStreamSynchronize(st));
+        trailing = std::sqrt(t2);
+        if (trailing <= o.tol * a_fro) { stopped = true; break; }
+      }
+    } else {
+      // ---- final block: economical SVD of T(r0:m, r0:n)
+      final_block = true;
+      r0f = r0; mif = mi; nif = ni;
+      if (mi > ni) {
+        final_tall = true;
+        double* Wf = uv ? (w.Wu_all + p.off_u[i - 1]) : w.Vu;
+        int64_t ldwf = uv ? mi : m;
+        copy_matrix(st, mi, ni, X, m, Wf, ldwf);
+        check_qr(panel_qr(st, mi, ni, Wf, ldwf, w.Rfin, ni, w.tau, w.Tu + size_t(p.nrand) * b * b, ni, w.qw));
+      } else {
+        copy_matrix(st, ni, ni, X, m, w.Rfin, ni);
+      }
+      k_done = n;
+      break;
+    }
+  }
+  if (!final_block && !stopped) k_done = std::min(k_done, n);
+
+  // ---- batched small SVDs
+  int max_sweeps = 0;
+  if (steps > 0)
+    jacobi_svd_batched(st, (int)steps, (int)b, w.Rall, b, b * b, w.Dall, w.Usall, w.Vsall, w.jwork, w.sweeps);
+  if (final_block)
+    jacobi_svd_batched(st, 1, (int)nif, w.Rfin, nif, nif * nif, w.Dfin, w.Usfin, w.Vsfin, w.jworkf,
+                       w.sweeps + steps);
+
+  // ---- folds into T (deferred)
+  for (int64_t si = 0; si < steps; ++si) {
+    const int64_t r0 = b * si;
+    const double* Us = w.Usall + size_t(si) * b * b;
+    const double* Vs = w.Vsall + size_t(si) * b * b;
+    write_diag_block(st, b, b, w.Dall + si * b, T + r0 + r0 * m, m);            // T(I2,J2) = D
+    const int64_t nc = n - r0 - b;
+    if (nc > 0) {                                                                // T(I2,J3) = Us^T T(I2,J3)
+      dg(w, st, true, false, b, nc, b, 1.0, Us, b, T + r0 + (r0 + b) * m, m, 0.0, w.fold, b);
+      copy_matrix(st, b, nc, w.fold, b, T + r0 + (r0 + b) * m, m);
+    }
+    if (r0 > 0) {                                                                // T(I1,J2) = T(I1,J2) Vs
+      dg(w, st, false, false, r0, b, b, 1.0, T + r0 * m, m, Vs, b, 0.0, w.fold, r0);
+      copy_matrix(st, r0, b, w.fold, r0, T + r0 * m, m);
+    }
+  }
+  if (final_block) {
+    write_diag_block(st, mif, nif, w.Dfin, T + r0f + r0f * m, m);               // [diag(D); 0]
+    if (r0f > 0) {
+      dg(w, st, false, false, r0f, nif, nif, 1.0, T + r0f * m, m, w.Vsfin, nif, 0.0, w.fold, r0f);
+      copy_matrix(st, r0f, nif, w.fold, r0f, T + r0f * m, m);
+    }
+  }
+
+  // ---- U, V by backward accumulation
+  if (uv) {
+    set_identity(st, n, n, V, n);
+    set_identity(st, m, m, U, m);
+    if (final_block && final_tall) {
+      const double* Wf = w.Wu_all + p.off_u[p.s - 1];
+      const double* Tf = w.Tu + size_t(p.nrand) * b * b;
+      double* Ub = U + r0f + r0f * m;
+      dg(w, st, true, false, nif, mif, mif, 1.0, Wf, mif, Ub, m, 0.0, w.fold, nif);   // Wf^T U'
+      dg(w, st, false, false, nif, mif, nif, 1.0, Tf, nif, w.fold, nif, 0.0, w.P, nif);  // Tf (.)
+      dg(w, st, false, false, mif, mif, nif, -1.0, Wf, mif, w.P, nif, 1.0, Ub, m);      // U' -= Wf (.)
+    }
+    for (int64_t si = steps - 1; si >= 0; --si) {
+      const int64_t r0 = b * si, mi = m - r0, ni = n - r0;
+      const double* Wv = w.Wv_all + p.off_v[si];
+      const double* Wu = w.Wu_all + p.off_u[si];
+      const double* Tv = w.Tv + size_t(si) * b * b;
+      const double* Tu = w.Tu + size_t(si) * b * b;
+      double* Vb = V + r0 + r0 * n;
+      double* Ub = U + r0 + r0 * m;
+      // V' <- (I - Wv Tv Wv^T) V'
+      dg(w, st, true, false, b, ni, ni, 1.0, Wv, ni, Vb, n, 0.0, w.Wt, b);
+      dg(w, st, false, false, b, ni, b, 1.0, Tv, b, w.Wt, b, 0.0, w.Wt2, b);
+      dg(w, st, false, false, ni, ni, b, -1.0, Wv, ni, w.Wt2, b, 1.0, Vb, n);
+      // U' <- (I - Wu Tu Wu^T) U'
+      dg(w, st, true, false, b, mi, mi, 1.0, Wu, mi, Ub, m, 0.0, w.fold, b);
+      dg(w, st, false, false, b, mi, b, 1.0, Tu, b, w.fold, b, 0.0, w.P, b);
+      dg(w, st, false, false, mi, mi, b, -1.0, Wu, mi, w.P, b, 1.0, Ub, m);
+    }
+    // column folds with the small SVD factors
+    for (int64_t si = 0; si < steps; ++si) {
+      const int64_t r0 = b * si;
+      dg(w, st, false, false, m, b, b, 1.0, U + r0 * m, m, w.Usall + size_t(si) * b * b, b, 0.0, w.fold, m);
+      copy_matrix(st, m, b, w.fold, m, U + r0 * m, m);
+      dg(w, st, false, false, n, b, b, 1.0, V + r0 * n, n, w.Vsall + size_t(si) * b * b, b, 0.0, w.fold, n);
+      copy_matrix(st, n, b, w.fold, n, V + r0 * n, n);
+    }
+    if (final_block) {
+      dg(w, st, false, false, m, nif, nif, 1.0, U + r0f * m, m, w.Usfin, nif, 0.0, w.fold, m);
+      copy_matrix(st, m, nif, w.fold, m, U + r0f * m, m);
+      dg(w, st, false, false, n, nif, nif, 1.0, V + r0f * n, n, w.Vsfin, nif, 0.0, w.fold, n);
+      copy_matrix(st, n, nif, w.fold, n, V + r0f * n, n);
+    }
+  }
+
+  if (info) {
+    info->k_done = k_done;
+    info->steps = (int32_t)steps;
+    info->final_block = final_block ? 1 : 0;
+    info->a_fro = a_fro;
+    int nsw = (int)steps + (final_block ? 1 : 0);
+    std::vector<int> sw(std::max(nsw, 1), 0);
+    if (nsw > 0) {
+      RUTV_CK(cudaMemcpyAsync(sw.data(), w.sweeps, sizeof(int) * nsw, cudaMemcpyDeviceToHost, st));
+    }
+    if (k_done < n) {
+      double t2 = 0.0;
+      fro2(st, m - k_done, n - k_done, T + k_done + k_done * m, m, w.nrm, w.scal);
+      RUTV_CK(cudaMemcpyAsync(&t2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+      RUTV_CK(cudaStreamSynchronize(st));
+      info->trailing_fro = std::sqrt(t2);
+    } else {
+      RUTV_CK(cudaStreamSynchronize(st));
+      info->trailing_fro = 0.0;
+    }
+    info->max_sweeps = 0;
+    for (int v : sw) info->max_sweeps = std::max(info->max_sweeps, v);
+  }
+  (void)trailing;
+  return RANDUTV_OK;
+}
+
+void* cached_ws(size_t bytes) {
+  if (bytes > g_ws_bytes) {
+    if (g_ws) {
+      cudaDeviceSynchronize();
+      cudaFree(g_ws);
+      g_ws = nullptr;
+      g_ws_bytes = 0;
+    }
+    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      g_ws = nullptr;
+      return nullptr;
+    }
+    g_ws_bytes = bytes;
+  }
+  return g_ws;
+}
+
+int validate(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, int64_t k_stop, double* U,
+             double* T, double* V) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (!A) return -3;
+  if (lda < m) return -4;
+  if (b < 1 || b > RANDUTV_MAX_B) return -5;
+  if (q < 0) return -6;
+  if (k_stop < 0) return -8;
+  if ((U == nullptr) != (V == nullptr)) return -9;
+  if (!T) return -10;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* randutv_version(void) { return "randutv-b200 0.1 (sm_100a, DMMA fp64)"; }
+
+const char* randutv_strerror(int code) {
+  switch (code) {
+    case RANDUTV_OK: return "success";
+    case RANDUTV_ERR_NONFINITE: return "input holds NaN or Inf";
+    case RANDUTV_ERR_CUDA: return "CUDA runtime error";
+    case RANDUTV_ERR_NOMEM: return "device allocation failed";
+    case RANDUTV_ERR_NCCL: return "NCCL error";
+    case RANDUTV_ERR_UNSUPPORTED: return "unsupported shape for this build";
+    default: break;
+  }
+  if (code < 0) return "invalid argument (-code = 1-based position in randutv_factor)";
+  return "unknown error";
+}
+
+size_t randutv_workspace_size(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv) {
+  if (m < 1 || n < 1 || b < 1) return 0;
+  b = std::min<int64_t>(b, std::max(m, n));
+  return workspace_bytes(make_plan(m, n, b, q, with_uv != 0));
+}
+
+int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
+                      int32_t q, uint64_t seed, int64_t k_stop, double* U, double* T, double* V,
+                      randutv_info* info) {
+  int rc = validate(m, n, A, lda, b, q, k_stop, U, T, V);
+  if (rc) return rc;
+  randutv_opts o{};
+  if (opts) o = *opts;
+  if (o.tol < 0 || std::isnan(o.tol)) return -12;
+  if (b > n) b = n;  // a single final-SVD step, same result as any b >= n
+  std::lock_guard<std::mutex> lock(g_mu);
+  try {
+    const bool host = mem_kind(A) == MEM_HOST || mem_kind(T) == MEM_HOST || (U && mem_kind(U) == MEM_HOST) ||
+                      (V && mem_kind(V) == MEM_HOST);
+    cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+    const size_t need = workspace_bytes(make_plan(m, n, b, q, U != nullptr));
+    void* ws = o.workspace;
+    size_t wsb = o.workspace_bytes;
+    if (!ws) {
+      ws = cached_ws(need);
+      wsb = need;
+      if (!ws) return RANDUTV_ERR_NOMEM;
+    } else if (wsb < need) {
+      return -12;
+    }
+    if (!host) return factor_device(o, m, n, A, lda, b, q, seed, k_stop, U, T, V, info, ws, wsb);
+    // host buffers: stage through device memory inside the call
+    double *dT = nullptr, *dU = nullptr, *dV = nullptr;
+    if (cudaMalloc(&dT, sizeof(double) * m * n) != cudaSuccess) return RANDUTV_ERR_NOMEM;
+    if (U && (cudaMalloc(&dU, sizeof(double) * m * m) != cudaSuccess ||
+              cudaMalloc(&dV, sizeof(double) * n * n) != cudaSuccess)) {
+      cudaFree(dT); cudaFree(dU);
+      return RANDUTV_ERR_NOMEM;
+    }
+    RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
+                              cudaMemcpyDefault, st));
+    rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb);
+    if (rc == RANDUTV_OK) {
+      RUTV_CK(cudaMemcpyAsync(T, dT, sizeof(double) * m * n, cudaMemcpyDefault, st));
+      if (U) {
+        RUTV_CK(cudaMemcpyAsync(U, dU, sizeof(double) * m * m, cudaMemcpyDefault, st));
+        RUTV_CK(cudaMemcpyAsync(V, dV, sizeof(double) * n * n, cudaMemcpyDefault, st));
+      }
+    }
+    RUTV_CK(cudaStreamSynchronize(st));
+    cudaFree(dT);
+    if (dU) cudaFree(dU);
+    if (dV) cudaFree(dV);
+    return rc;
+  } catch (const CudaError& e) {
+    fprintf(stderr, "randutv: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);
+    return e.e == cudaErrorMemoryAllocation ? RANDUTV_ERR_NOMEM : RANDUTV_ERR_CUDA;
+  } catch (int code) {
+    return code;
+  }
+}
+
+int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, uint64_t seed,
+                   int64_t k_stop, double* U, double* T, double* V) {
+  randutv_opts o{};
+  int rc = randutv_factor_ex(&o, m, n, A, lda, b, q, seed, k_stop, U, T, V, nullptr);
+  if (rc == 0 && cudaStreamSynchronize(cudaStreamPerThread) != cudaSuccess) return RANDUTV_ERR_CUDA;
+  return rc;
+}
+
+int randutv_gaussian(double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed, uint32_t step,
+                     uint32_t purpose, void* stream) {
+  if (!G) return -1;
+  if (ldg < rows) return -2;
+  if (rows < 0) return -3;
+  if (cols < 0) return -4;
+  try {
+    gaussian_fill(stream ? (cudaStream_t)stream : cudaStreamPerThread, G, ldg, rows, cols, seed, step, purpose);
+  } catch (const CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+  return 0;
+}
+
+int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  if (M < 0) return -3;
+  if (N < 0) return -4;
+  if (K < 0) return -5;
+  if (lda < std::max<int64_t>(1, transa ? K : M)) return -8;
+  if (ldb < std::max<int64_t>(1, transb ? N : K)) return -10;
+  if (ldc < std::max<int64_t>(1, M)) return -13;
+  std::lock_guard<std::mutex> lock(g_mu);
+  try {
+    size_t part = size_t(8) * std::max<int64_t>(M, 1) * std::max<int64_t>(N, 1) + size_t(148) * 32 * 1024;
+    part = std::min(part, size_t(1) << 30);
+    double* ws = (double*)cached_ws(part * sizeof(double));
+    if (!ws) return RANDUTV_ERR_NOMEM;
+    dgemm(stream ? (cudaStream_t)stream : cudaStreamPerThread, transa != 0, transb != 0, M, N, K, alpha, A, lda, B,
+          ldb, beta, C, ldc, ws, part);
+  } catch (const CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+  return 0;
+}
+
+int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                     double* Tw, int64_t ldt, void* stream) {
+  if (b < 1 || b > RANDUTV_MAX_B) return -2;
+  if (m < b) return -1;
+  if (!V || ldv < m) return -4;
+  if (!R || ldr < b) return -6;
+  if (!tau) return -7;
+  if (!Tw || ldt < b) return -9;
+  std::lock_guard<std::mutex> lock(g_mu);
+  try {
+    size_t part = size_t(8) * m * b + size_t(148) * 32 * 1024;
+    size_t extra = size_t(3) * 32 * b + 1024;
+    double* ws = (double*)cached_ws((part + extra) * sizeof(double));
+    if (!ws) return RANDUTV_ERR_NOMEM;
+    QrWork w{ws, part, ws + part, ws + part + 32 * b, ws + part + 64 * b};
+    return panel_qr(stream ? (cudaStream_t)stream : cudaStreamPerThread, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
+  } catch (const CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+}
+
+int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,
+                              double* Us, double* Vs, int32_t* sweeps, void* stream) {
+  if (batch < 0) return -1;
+  if (k < 1 || k > RANDUTV_MAX_B) return -2;
+  if (!R || ldr < k) return -4;
+  std::lock_guard<std::mutex> lock(g_mu);
+  try {
+    size_t need = jacobi_work_elems(batch, k);
+    double* ws = (double*)cached_ws(need * sizeof(double));
+    if (!ws) return RANDUTV_ERR_NOMEM;
+    jacobi_svd_batched(stream ? (cudaStream_t)stream : cudaStreamPerThread, batch, k, R, ldr, strideR, D, Us, Vs,
+                       ws, sweeps);
+  } catch (const CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Internal host-side launchers of the randUTV sm_100a kernels (not the C-ABI;
+// see include/randutv.h for that).  All matrices fp64 column-major, device
+// pointers, asynchronous on the given stream.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace rutv {
+
+int num_sms();
+
+// ---- gemm.cu -------------------------------------------------------------
+// C = alpha op(A) op(B) + beta C.  ``part`` (part_elems doubles) is the split-K
+// scratch; force_splits > 0 overrides the split heuristic.
+void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* part,
+           size_t part_elems, int force_splits = 0);
+int gemm_choose_splits(int64_t M, int64_t N, int64_t K, size_t part_elems);
+
+// ---- misc.cu ---------------------------------------------------------------
+void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc);
+void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd);
+void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd);  // D = I (m x n)
+void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd);
+// Copy S -> D (may alias when equal), accumulate sum of squares and a
+// non-finite flag.  out2[0] = ||S||_F^2 (deterministic two-pass), flag[0] != 0 if any
+// entry is NaN/Inf.  ``scratch`` needs 4096 doubles.
+void copy_norm_check(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D,
+                     int64_t ldd, double* scratch, double* out2, int* flag);
+// sum of squares of an m x n block into out2[0] (deterministic).
+void fro2(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* scratch, double* out2);
+// Philox4x32-10 Gaussian block (R2).
+void gaussian_fill(cudaStream_t st, double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed,
+                   uint32_t step, uint32_t purpose);
+// D = diag(d) on a k x k block (exact zeros off the diagonal) below which rows
+// [k, m) of the same columns are zeroed.
+void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, double* D, int64_t ldd);
+
+// ---- qr.cu -----------------------------------------------------------------
+struct QrWork {
+  double* part;      // split-K scratch for the inner GEMMs
+  size_t part_elems;
+  double* sfull;     // b_leaf x b   (V_l^T [V_prev | V_l | A_rest])
+  double* s2;        // b_leaf x b
+  double* z;         // b x b_leaf
+};
+size_t qr_work_elems(int64_t b);
+// Householder QR of the m x b panel held in V (ld ldv), in place:
+// on exit V is the explicit unit-lower-trapezoidal reflector matrix, R (b x b,
+// ld ldr) the upper-triangular factor (zeros below), tau[b] the reflector
+// scalars and Tw (b x b, ld ldt) the forward compact-WY factor:
+// H_1 ... H_b = I - V Tw V^T.  LAPACK dlarfg sign convention (R3).
+int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+             double* Tw, int64_t ldt, const QrWork& w);
+// Q1 = (I - V Tw V^T)[:, :b] (thin explicit Q), written to Q (m x b).
+void thin_q(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const double* Tw, int64_t ldt,
+            double* Q, int64_t ldq, double* tmp_bb, double* part, size_t part_elems);
+int qr_max_rows();
+
+// ---- jacobi.cu -------------------------------------------------------------
+// Batched one-sided Jacobi SVD of ``batch`` k x k matrices R_i (R_i at
+// R + i*strideR, ld ldr):  R_i = Us_i diag(D_i) Vs_i^T, D_i non-increasing.
+// Works on B = R_i^T.  work needs 2*batch*k*k doubles.
+size_t jacobi_work_elems(int batch, int k);
+void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
+                        double* D, double* Us, double* Vs, double* work, int* sweeps_out);
+
+}  // namespace rutv

@@ -1,0 +1,158 @@
+// Memory-bound helpers: copies, identity/zero fills, Frobenius norms with a
+// non-finite scan (input validation), the Philox Gaussian draw.
+#include "common.cuh"
+#include "kernels.h"
+#include "philox.cuh"
+
+#include <algorithm>
+
+namespace rutv {
+
+namespace {
+constexpr int TB = 256;
+
+inline int grid_for(int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, TB), int64_t(num_sms()) * 16));
+}
+
+__global__ void scale_k(int64_t m, int64_t n, double beta, double* C, int64_t ldc) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+      C[i + j * ldc] = beta == 0.0 ? 0.0 : beta * C[i + j * ldc];
+}
+
+__global__ void copy_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds, double* __restrict__ D,
+                       int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+      D[i + j * ldd] = S[i + j * lds];
+}
+
+__global__ void ident_k(int64_t m, int64_t n, double* D, int64_t ldd, double diagv) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+      D[i + j * ldd] = (i == j) ? diagv : 0.0;
+}
+
+// Per-block partial sums of squares (fixed partition -> deterministic).
+__global__ void norm_partial_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds,
+                               double* __restrict__ D, int64_t ldd, double* partials, int* flag) {
+  __shared__ double red[TB / 32];
+  const int64_t total = m * n;
+  double acc = 0.0;
+  int bad = 0;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t i = idx % m, j = idx / m;
+    double v = S[i + j * lds];
+    if (D) D[i + j * ldd] = v;
+    if (!isfinite(v)) bad = 1;
+    acc = fma(v, v, acc);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  if (bad && flag) atomicOr(flag, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TB / 32; ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void norm_final_k(int nparts, const double* partials, double* out2) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += partials[i];
+    out2[0] = s;
+  }
+}
+
+__global__ void gaussian_k(double* G, int64_t ldg, int64_t rows, int64_t cols, uint32_t k0, uint32_t k1,
+                           uint32_t step, uint32_t purpose) {
+  const int64_t npairs = (rows + 1) / 2;
+  const int64_t total = npairs * cols;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t p = idx % npairs, c = idx / npairs;
+    double g0, g1;
+    philox_gaussian_pair(uint32_t(p), uint32_t(c), step, purpose, k0, k1, g0, g1);
+    G[2 * p + c * ldg] = g0;
+    if (2 * p + 1 < rows) G[2 * p + 1 + c * ldg] = g1;
+  }
+}
+
+__global__ void diag_block_k(int64_t m, int64_t k, const double* d, double* D, int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y)
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+      D[i + j * ldd] = (i == j) ? d[j] : 0.0;
+}
+
+dim3 grid2(int64_t m, int64_t n) {
+  int gx = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(m, TB), 64));
+  int gy = (int)std::max<int64_t>(1, std::min<int64_t>(n, 4096));
+  return dim3(gx, gy);
+}
+}  // namespace
+
+void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc) {
+  if (m <= 0 || n <= 0) return;
+  scale_k<<<grid2(m, n), TB, 0, st>>>(m, n, beta, C, ldc);
+  RUTV_LAUNCH_CK();
+}
+
+void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
+  if (m <= 0 || n <= 0 || S == D) return;
+  copy_k<<<grid2(m, n), TB, 0, st>>>(m, n, S, lds, D, ldd);
+  RUTV_LAUNCH_CK();
+}
+
+void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
+  if (m <= 0 || n <= 0) return;
+  ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 1.0);
+  RUTV_LAUNCH_CK();
+}
+
+void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
+  if (m <= 0 || n <= 0) return;
+  ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 0.0);
+  RUTV_LAUNCH_CK();
+}
+
+void copy_norm_check(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D,
+                     int64_t ldd, double* scratch, double* out2, int* flag) {
+  int blocks = std::min(grid_for(m * n), 4096);
+  norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag);
+  RUTV_LAUNCH_CK();
+  norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2);
+  RUTV_LAUNCH_CK();
+}
+
+void fro2(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* scratch, double* out2) {
+  if (m <= 0 || n <= 0) {
+    RUTV_CK(cudaMemsetAsync(out2, 0, sizeof(double), st));
+    return;
+  }
+  int blocks = std::min(grid_for(m * n), 4096);
+  norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, nullptr, 0, scratch, nullptr);
+  RUTV_LAUNCH_CK();
+  norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2);
+  RUTV_LAUNCH_CK();
+}
+
+void gaussian_fill(cudaStream_t st, double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed,
+                   uint32_t step, uint32_t purpose) {
+  if (rows <= 0 || cols <= 0) return;
+  int64_t total = ((rows + 1) / 2) * cols;
+  gaussian_k<<<grid_for(total), TB, 0, st>>>(G, ldg, rows, cols, uint32_t(seed & 0xffffffffu),
+                                             uint32_t(seed >> 32), step, purpose);
+  RUTV_LAUNCH_CK();
+}
+
+void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, double* D, int64_t ldd) {
+  if (m <= 0 || k <= 0) return;
+  diag_block_k<<<grid2(m, k), TB, 0, st>>>(m, k, d, D, ldd);
+  RUTV_LAUNCH_CK();
+}
+
+}  // namespace rutv

@@ -1,0 +1,230 @@
+"""GPU parity: every CUDA kernel and the whole factorization, through the C ABI,
+against the oracle on the same seeded inputs (DESIGN.md §"Parity")."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_1703_00998_b200 as P  # noqa: E402
+import testmat  # noqa: E402
+from util import EPS, check_parity, diag_blocks_ok, ek_fro, invariants  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def to_dev(A: np.ndarray):
+    """Column-major device copy of a host matrix."""
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(A).T)).to(DEV).t()
+
+
+def to_host(X):
+    return X.detach().cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- Philox G
+@pytest.mark.parametrize("rows,cols,seed,step", [(1, 1, 0, 0), (501, 50, 0, 3), (10000, 256, 3, 17),
+                                                 (7, 5, 2**40 + 5, 1)])
+def test_gaussian_matches_oracle(rows, cols, seed, step):
+    g = to_host(P.gaussian(rows, cols, seed, step))
+    r = oracle.gaussian_block(seed, step, rows, cols)
+    ulp = np.spacing(np.abs(r))
+    assert np.all(np.abs(g - r) <= 4 * ulp)            # transcendental libm vs CUDA: <= 4 ulp
+    assert np.mean(g == r) > 0.5                        # most entries bitwise equal
+
+
+# ----------------------------------------------------------------------------- DMMA GEMM
+GEMM_CASES = [
+    # (M, N, K, ta, tb)
+    (1, 1, 1, False, False), (37, 29, 41, False, False), (130, 257, 33, True, False), (255, 129, 300, False, True),
+    (128, 128, 16, True, True), (2000, 256, 3000, True, False), (32, 256, 10000, True, False),
+    (3001, 513, 256, False, True), (64, 64, 0, False, False),
+]
+
+
+@pytest.mark.parametrize("M,N,K,ta,tb", GEMM_CASES)
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_dgemm_vs_oracle_matmul(M, N, K, ta, tb, beta):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((N, K) if tb else (K, N))
+    C0 = rng.standard_normal((M, N))
+    alpha = -1.25
+    ref = alpha * (A.T if ta else A) @ (B.T if tb else B) + beta * C0
+    C = to_dev(C0)
+    P.dgemm(ta, tb, alpha, to_dev(A), to_dev(B), beta, C)
+    got = to_host(C)
+    bound = (K + 2) * EPS * (np.abs(A.T if ta else A) @ np.abs(B.T if tb else B) * abs(alpha) + abs(beta) * np.abs(C0))
+    assert np.all(np.abs(got - ref) <= 2 * bound + 1e-300)
+
+
+def test_dgemm_misaligned_views():
+    """Odd leading dimensions and odd offsets take the 8-byte load path."""
+    rng = np.random.default_rng(1)
+    big = to_dev(rng.standard_normal((301, 203)))
+    A = big[1:150, 3:120]            # 149 x 117, ld 301, odd offset
+    B = big[5:122, 7:40]             # 117 x 33
+    C = torch.zeros(149, 33, dtype=torch.float64, device=DEV).t().contiguous().t()
+    P.dgemm(False, False, 1.0, A, B, 0.0, C)
+    ref = to_host(A) @ to_host(B)
+    np.testing.assert_allclose(to_host(C), ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+
+
+# ----------------------------------------------------------------------------- Householder panel QR
+@pytest.mark.parametrize("m,b", [(40, 8), (500, 50), (1000, 77), (3000, 128), (10000, 256), (20000, 64)])
+def test_panel_qr_vs_oracle(m, b):
+    rng = np.random.default_rng(m + b)
+    Y = rng.standard_normal((m, b)) @ np.diag(10.0 ** -np.linspace(0, 3, b))
+    V, R, tau, Tw = P.panel_qr(to_dev(Y))
+    F, tau_o = oracle.geqr2(Y)
+    Vo = oracle.unit_lower(F, b)
+    To = oracle.larft(Vo, tau_o)
+    Ro = np.triu(F[:b, :b])
+    np.testing.assert_allclose(to_host(tau), tau_o, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(to_host(V), Vo, rtol=0, atol=1e-10 * max(1, np.abs(Vo).max()))
+    np.testing.assert_allclose(to_host(R), Ro, rtol=0, atol=1e-12 * np.abs(Ro).max())
+    np.testing.assert_allclose(to_host(Tw), To, rtol=0, atol=1e-10 * max(1, np.abs(To).max()))
+    Vh, Th = to_host(V), to_host(Tw)
+    assert np.all(np.triu(Vh, 1) == 0) and np.all(np.diag(Vh) == 1) and np.all(np.tril(to_host(R), -1) == 0)
+    # orthogonality of the compact-WY product and reconstruction Y = Q [R; 0]
+    Q1 = np.eye(m, b) - Vh @ (Th @ Vh[:b].T)
+    assert np.linalg.norm(Q1.T @ Q1 - np.eye(b)) < 1e-13 * math.sqrt(m) * 10
+    assert np.linalg.norm(Q1 @ to_host(R) - Y) <= 1e-13 * np.linalg.norm(Y) * 10
+
+
+def test_panel_qr_degenerate_columns():
+    """Zero and repeated columns: tau = 0 reflectors (H = I), still exact."""
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((300, 40))
+    Y[:, 5] = 0.0
+    Y[:, 9] = Y[:, 8]
+    Y[:, 30:] = 0.0
+    V, R, tau, Tw = P.panel_qr(to_dev(Y))
+    F, tau_o = oracle.geqr2(Y)
+    np.testing.assert_allclose(to_host(tau)[:5], tau_o[:5], atol=1e-13)
+    assert np.all(to_host(tau)[30:] == 0.0)
+    Vh, Th = to_host(V), to_host(Tw)
+    Q1 = np.eye(300, 40) - Vh @ (Th @ Vh[:40].T)
+    assert np.linalg.norm(Q1 @ to_host(R) - Y) <= 1e-12 * np.linalg.norm(Y)
+
+
+# ----------------------------------------------------------------------------- batched Jacobi SVD
+@pytest.mark.parametrize("k,batch", [(1, 2), (2, 3), (50, 4), (128, 3), (256, 2), (512, 1)])
+def test_small_svd_batched_vs_lapack(k, batch):
+    rng = np.random.default_rng(k)
+    Rs = np.stack([np.triu(rng.standard_normal((k, k))) @ np.diag(10.0 ** -np.linspace(0, 5 * (i % 2), k))
+                   for i in range(batch)])
+    D, Us, Vs, sw = P.small_svd_batched(torch.from_numpy(Rs).to(DEV))
+    D, Us, Vs = to_host(D), to_host(Us), to_host(Vs)
+    for i in range(batch):
+        s = oracle.small_svd(Rs[i])[1]
+        np.testing.assert_allclose(D[i], s, rtol=0, atol=1e-13 * s[0] * max(1, k / 64))
+        assert np.all(np.diff(D[i]) <= 0)
+        assert np.linalg.norm(Us[i].T @ Us[i] - np.eye(k)) < 1e-12 * k
+        assert np.linalg.norm(Vs[i].T @ Vs[i] - np.eye(k)) < 1e-12 * k
+        assert np.linalg.norm(Us[i] @ np.diag(D[i]) @ Vs[i].T - Rs[i]) < 1e-13 * k * np.linalg.norm(Rs[i])
+    assert to_host(sw).max() <= 40
+
+
+def test_small_svd_closed_forms_and_zero():
+    R = np.stack([np.array([[1.0, 1.0], [0.0, 1.0]]), np.zeros((2, 2)), np.array([[0.0, 1.0], [1.0, 0.0]])])
+    D, Us, Vs, _ = P.small_svd_batched(torch.from_numpy(R).to(DEV))
+    D, Us, Vs = to_host(D), to_host(Us), to_host(Vs)
+    np.testing.assert_allclose(D[0], [(1 + 5 ** 0.5) / 2, (5 ** 0.5 - 1) / 2], rtol=1e-15)
+    assert np.all(D[1] == 0)
+    np.testing.assert_allclose(Vs[1].T @ Vs[1], np.eye(2), atol=1e-15)   # completed basis
+    np.testing.assert_allclose(D[2], [1, 1], rtol=1e-15)
+    for i in range(3):
+        np.testing.assert_allclose(Us[i] @ np.diag(D[i]) @ Vs[i].T, R[i], atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- whole factorization
+PARITY = [
+    # name, scale, q override, with_uv
+    ("c1", 1.0, None, True),      # BASELINE config 1 itself: 500 x 500, b=50, q=1
+    ("c2", 0.2, 0, True),         # 600 x 600 exponential decay, b=128, q = 0/1/2
+    ("c2", 0.2, 1, False),
+    ("c2", 0.2, 2, True),
+    ("c3", 0.1, None, False),     # 1000 x 1000 S-shape, b=125, q=2
+    ("c4", 0.05, None, True),     # 1000 x 400 tall Gaussian, b=50, q=1 (tall final block)
+]
+
+
+@pytest.mark.parametrize("name,scale,q,uv", PARITY)
+def test_randutv_parity(name, scale, q, uv):
+    c = testmat.config(name, scale=scale, q=q)
+    A = c.A
+    m, n = A.shape
+    ref = oracle.randutv(A, c.b, c.q, c.seed, build_ortho=uv)
+    U, T, V, info = P.randutv(to_dev(A), c.b, c.q, c.seed, with_uv=uv)
+    torch.cuda.synchronize()
+    Th = to_host(T)
+    par = check_parity(Th, ref["T"], ref["a_fro"])
+    assert par["diag_ok"], par
+    assert par["ek_ok"], par
+    assert info.k_done == n and info.steps == ref["steps"]
+    assert np.all(np.tril(Th, -1) == 0.0)
+    assert diag_blocks_ok(Th, c.b, n)
+    inv = invariants(A, to_host(U) if uv else None, Th, to_host(V) if uv else None)
+    assert inv["fro_rel"] <= n * EPS * 4
+    if uv:
+        assert inv["recon"] <= 1e-13 * n
+        assert inv["orth_u"] <= 1e-13 * n and inv["orth_v"] <= 1e-13 * n
+
+
+def test_randutv_ragged_and_b_geq_n():
+    A = testmat.gaussian(333, 150, 11)
+    for b in (32, 150, 400):
+        ref = oracle.randutv(A, b, 1, 5)
+        U, T, V, info = P.randutv(to_dev(A), b, 1, 5)
+        par = check_parity(to_host(T), ref["T"], ref["a_fro"])
+        assert par["diag_ok"] and par["ek_ok"], (b, par)
+        inv = invariants(A, to_host(U), to_host(T), to_host(V))
+        assert inv["recon"] < 1e-13 * 150 and inv["tril_max"] == 0
+
+
+def test_randutv_early_stop_c5_like():
+    """Config-5 shape at small scale: low rank + 1e-8 noise, k_stop and tol."""
+    c = testmat.config("c5", scale=0.05)     # 1500 x 1500, rank 100, b=93, k_stop 102 -> k = 186
+    ref = oracle.randutv(c.A, c.b, c.q, c.seed, k_stop=c.k_stop, tol=c.tol, build_ortho=False)
+    U, T, V, info = P.randutv(to_dev(c.A), c.b, c.q, c.seed, k_stop=c.k_stop, tol=c.tol, with_uv=False)
+    Th = to_host(T)
+    assert info.k_done == ref["k"] and info.steps == ref["steps"]
+    k = info.k_done
+    assert np.all(Th[k:, :k] == 0)
+    np.testing.assert_allclose(np.abs(np.diag(Th)[:k]), np.abs(np.diag(ref["T"])[:k]), rtol=1e-10,
+                               atol=c.A.shape[0] * EPS * ref["a_fro"])
+    assert abs(info.trailing_fro - ref["trailing_fro"]) <= 1e-8 * ref["trailing_fro"] + 1e3 * EPS * ref["a_fro"]
+
+
+def test_identity_zero_and_nonfinite():
+    n = 96
+    U, T, V, _ = P.randutv(to_dev(np.eye(n)), 16, 1, 0)
+    np.testing.assert_allclose(to_host(T), np.eye(n), atol=1e-13)
+    U, T, V, _ = P.randutv(to_dev(np.zeros((n, n))), 16, 1, 0)
+    assert np.all(to_host(T) == 0)
+    assert np.linalg.norm(to_host(U).T @ to_host(U) - np.eye(n)) < 1e-12
+    bad = np.ones((n, n)); bad[3, 4] = np.nan
+    with pytest.raises(P.RandUTVError) as e:
+        P.randutv(to_dev(bad), 16, 1, 0)
+    assert e.value.code == 1
+
+
+def test_host_buffers_match_device():
+    """The C ABI on host buffers (staged inside the call) gives the same bits."""
+    c = testmat.config("c1", scale=0.4)
+    Uh, Th, Vh, _ = P.randutv(np.asfortranarray(c.A), c.b, c.q, c.seed)
+    U, T, V, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed)
+    assert np.array_equal(Th, to_host(T)) and np.array_equal(Uh, to_host(U))
+
+
+def test_deterministic():
+    c = testmat.config("c2", scale=0.1)
+    _, T1, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
+    _, T2, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
+    assert torch.equal(T1, T2)
