@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""randUTV benchmark: BASELINE.json's metric on BASELINE.json's config 3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" = one full randUTV factorization (every row of SURVEY §8(a)) of the
+config-3 matrix: 10000 x 10000 fp64, S-shaped spectrum, b = 256, q = 2, in the
+paper's "no orthonormal matrices" mode (U = V = NULL) that the flop formula
+(5+2q) m n^2 - (3+2q) n^3/3 of PAPER.md:1203-1207 counts.  value = that flop
+count / device time, whole job (N independent replicas: DESIGN.md "Multi-GPU").
+The input (800 MB) is larger than L2 (126 MB) and is re-read from HBM every
+step; T is rewritten from A inside each step.
+
+Extra keys: e2e (same metric through the C ABI on pinned HOST buffers, H2D of A
+and D2H of T inside the timed region), roofline (dominant kernel class = the
+DMMA GEMMs, CUDA-event timed per launch inside the library), cpu_baseline (the
+oracle on a bounded sample, rank 0, N = 1), clocks, gpu_launches, utv (the
+same factorization with U and V formed, for context).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "randUTV fp64 GFLOP/s & time-to-factor n=10k, 1/2/4/8 B200, % of FP64 peak"
+UNIT = "GFLOP/s"
+# FP64 DMMA peak measured on this pool's B200 by tools/fp64_peaks.cu (profiles/r01_fp64_peaks.md);
+# MEASURED_PEAKS.json carries no fp64 entry.
+FP64_DMMA_PEAK_TFLOPS = 37.0
+FP64_CUBLAS_DGEMM_TFLOPS = 35.46
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-utv", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(case, m, n):
+    return {
+        "workload": f"{case.name}: {m}x{n} fp64, b={case.b}, q={case.q}, T-only (U=V=NULL), full factorization"
+        if case.name != "c5" else f"c5: {m}x{n}, b={case.b}, q={case.q}, k_stop={case.k_stop}",
+        "m": m, "n": n, "b": case.b, "q": case.q, "reortho": True, "mode": "T",
+        "flops_formula": "(5+2q)mn^2-(3+2q)n^3/3 (PAPER.md:1205)",
+        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB), re-read every step" % (m * n * 8 / 1e6),
+    }
+
+
+def flops_for(case, m, n):
+    from paper_1703_00998_b200 import flops
+    if case.k_stop:
+        return flops.flops_T_steps(m, n, case.b, case.q, case.k_stop)
+    return flops.flops_T(m, n, case.q)
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def oracle_sample(A_host, case, reps=1):
+    """The oracle as it stands on this host: the first randomized step of the
+    workload (k_stop = b, T-only).  Returns (GFLOP/s, seconds, flops, cores)."""
+    import numpy as np
+    from oracle import randutv as oracle_randutv
+    from paper_1703_00998_b200 import flops
+    m, n = A_host.shape
+    f = flops.flops_T_steps(m, n, case.b, case.q, k_stop=case.b)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] or [os.cpu_count()])
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle_randutv(A_host, case.b, case.q, case.seed, k_stop=case.b, build_ortho=False)
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    del np
+    return f / t / 1e9, t, f, cores
+
+
+def make_input(case_name, device, rank):
+    import testmat
+    At, case = testmat.device_config(case_name, device=device)
+    return At, case
+
+
+def run_reference(args):
+    """--impl reference: the oracle (CPU) on the same config, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    import testmat
+    case_name = args.config
+    if torch.cuda.is_available():
+        At, case = testmat.device_config(case_name, device="cuda")
+        A_host = np.asfortranarray(At.t().cpu().numpy())
+        del At
+        torch.cuda.empty_cache()
+    else:
+        c = testmat.config(case_name)
+        A_host, case = c.A, c
+    m, n = A_host.shape
+    for _ in range(max(args.warmup, 0)):
+        pass  # the oracle has no warm-up state; warm-up steps are skipped to bound the run time
+    vals, ts = [], []
+    for _ in range(args.steps):
+        v, t, f, cores = oracle_sample(A_host, case)
+        vals.append(v)
+        ts.append(t)
+    value = statistics.median(vals)
+    sample = f"first randomized step of {case_name} (k_stop=b={case.b}, q={case.q}, T-only) on the full {m}x{n} input"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(ts), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_desc(case, m, n),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import paper_1703_00998_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    At, case = make_input(args.config, dev, rank)
+    A = At.t()
+    m, n = A.shape
+    F = flops_for(case, m, n)
+    T = P.empty_cm(m, n, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(with_uv=False, out=None):
+        return P.randutv(A, case.b, case.q, case.seed, k_stop=case.k_stop, tol=case.tol, with_uv=with_uv,
+                         out=out if out is not None else (None, T, None))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------------------------------------------------------- timed region
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = P.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = P.launch_count() - l0
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * F / (ms * 1e-3) / 1e9
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel class
+    P.profile_begin()
+    step()
+    prof = P.profile_end()
+    g = prof["dmma_gemm"]
+    tot_ms = sum(v["ms"] for v in prof.values())
+    achieved = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roofline = {
+        "bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": traffic,
+        "kernel": "dgemm_kernel (FP64 DMMA m8n8k4) incl. split-K reduce",
+        "peak_source": "measured DMMA peak, tools/fp64_peaks.cu (profiles/r01_fp64_peaks.md); "
+                       "MEASURED_PEAKS.json has no fp64 entry",
+        "gemm_launches": g["launches"], "gemm_share_of_event_time": round(g["ms"] / tot_ms, 4) if tot_ms else None,
+        "breakdown_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+    }
+
+    # ---------------------------------------------------------------- U,V formed (context)
+    utv = None
+    if not args.no_utv and rank == 0:
+        U = P.empty_cm(m, m, dev)
+        V = P.empty_cm(n, n, dev)
+        step(True, (U, T, V))
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(True, (U, T, V))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tu = e0.elapsed_time(e1)
+        utv = {"ms": round(tu, 3), "gflops_credited_FT": round(F / (tu * 1e-3) / 1e9, 3),
+               "gflops_executed": round((F + P.flops.flops_UV(m, n)) / (tu * 1e-3) / 1e9, 3)}
+        del U, V
+        torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- end to end through the C ABI, host buffers
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+        Ah.copy_(At)
+        Th = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+        torch.cuda.synchronize(dev)
+        P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None, Th.data_ptr(), None)
+        if dist:
+            dist.barrier()
+        reps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            rc = P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None, Th.data_ptr(),
+                              None)
+            assert rc == 0, rc
+        te = (time.perf_counter() - t0) / reps
+        if dist:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": round(world * F / te / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": m * n * 8,
+               "d2h_bytes_per_step": m * n * 8, "ms_per_step": round(te * 1e3, 3),
+               "timer": "host wall clock around the synchronous randutv_factor call (pinned host A and T)"}
+        del Ah, Th
+
+    # ---------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        A_host = np.asfortranarray(A.cpu().numpy())
+        v, t, f, cores = oracle_sample(A_host, case)
+        cpu = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first randomized step of {case.name} (k_stop=b={case.b}, q={case.q}, T-only) "
+                         f"on the same {m}x{n} input: {f:.3e} flops in {t:.2f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(workload_desc(case, m, n), parallelism=f"replicas x{world}" if world > 1 else "single"),
+            "pct_fp64_peak": round(100 * value / world / 1e3 / FP64_DMMA_PEAK_TFLOPS, 2),
+            "pct_cublas_dgemm": round(100 * value / world / 1e3 / FP64_CUBLAS_DGEMM_TFLOPS, 2),
+            "time_to_factor_s": round(ms * 1e-3, 4),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "utv": utv,
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

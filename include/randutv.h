@@ -142,6 +142,21 @@ RANDUTV_API int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, d
 RANDUTV_API int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,
                               double* Us, double* Vs, int32_t* sweeps, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation (used by bench.py).
+ * ------------------------------------------------------------------------ */
+
+/* Total kernel launches issued by this library since it was loaded. */
+RANDUTV_API long long randutv_launch_count(void);
+
+/* Between begin and end every kernel launch is bracketed by CUDA events on its
+ * stream.  end synchronises the device and returns, per kernel class
+ * [0 = DMMA GEMM, 1 = panel-QR leaf, 2 = Jacobi SVD, 3 = memory-bound helpers],
+ * the summed event time in ms, the summed algorithmic flops (2MNK for GEMMs,
+ * 0 otherwise) and the launch count.  Arrays hold 4 entries (may be NULL). */
+RANDUTV_API int randutv_profile_begin(void);
+RANDUTV_API int randutv_profile_end(double* ms, double* flops, long long* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,10 @@ def lib():
                                 c_i64, c_vp]
     L.randutv_panel_qr.argtypes = [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]
     L.randutv_small_svd_batched.argtypes = [c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]
+    L.randutv_launch_count.restype = ctypes.c_longlong
+    L.randutv_profile_begin.restype = ctypes.c_int
+    L.randutv_profile_end.argtypes = [c_vp, c_vp, c_vp]
+    L.randutv_profile_end.restype = ctypes.c_int
     for f in ("randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_small_svd_batched"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -86,7 +90,28 @@ def lib():
 
 EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
             "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr",
-            "randutv_small_svd_batched"]
+            "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
+            "randutv_profile_end"]
+
+KERNEL_CLASSES = ("dmma_gemm", "panel_qr_leaf", "jacobi_svd", "memory_helpers")
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the library since load."""
+    return int(lib().randutv_launch_count())
+
+
+def profile_begin():
+    _check(lib().randutv_profile_begin(), "randutv_profile_begin")
+
+
+def profile_end() -> dict:
+    """Per-class event time (ms), algorithmic flops and launches since profile_begin()."""
+    ms = (ctypes.c_double * 4)()
+    fl = (ctypes.c_double * 4)()
+    ln = (ctypes.c_longlong * 4)()
+    _check(lib().randutv_profile_end(ms, fl, ln), "randutv_profile_end")
+    return {k: {"ms": ms[i], "flops": fl[i], "launches": ln[i]} for i, k in enumerate(KERNEL_CLASSES)}
 
 
 # --------------------------------------------------------------------------- layout helpers

@@ -34,6 +34,8 @@ namespace {
 std::mutex g_mu;
 void* g_ws = nullptr;
 size_t g_ws_bytes = 0;
+void* g_stage = nullptr;   // device staging for host-buffer calls
+size_t g_stage_bytes = 0;
 
 struct Plan {
   int64_t m, n, b;
@@ -391,6 +393,24 @@ void* cached_ws(size_t bytes) {
   return g_ws;
 }
 
+void* cached_stage(size_t bytes) {
+  if (bytes > g_stage_bytes) {
+    if (g_stage) {
+      cudaDeviceSynchronize();
+      cudaFree(g_stage);
+      g_stage = nullptr;
+      g_stage_bytes = 0;
+    }
+    if (cudaMalloc(&g_stage, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      g_stage = nullptr;
+      return nullptr;
+    }
+    g_stage_bytes = bytes;
+  }
+  return g_stage;
+}
+
 int validate(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, int64_t k_stop, double* U,
              double* T, double* V) {
   if (m < 1) return -1;
@@ -457,13 +477,12 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     }
     if (!host) return factor_device(o, m, n, A, lda, b, q, seed, k_stop, U, T, V, info, ws, wsb);
     // host buffers: stage through device memory inside the call
-    double *dT = nullptr, *dU = nullptr, *dV = nullptr;
-    if (cudaMalloc(&dT, sizeof(double) * m * n) != cudaSuccess) return RANDUTV_ERR_NOMEM;
-    if (U && (cudaMalloc(&dU, sizeof(double) * m * m) != cudaSuccess ||
-              cudaMalloc(&dV, sizeof(double) * n * n) != cudaSuccess)) {
-      cudaFree(dT); cudaFree(dU);
-      return RANDUTV_ERR_NOMEM;
-    }
+    const size_t elems = size_t(m) * n + (U ? size_t(m) * m + size_t(n) * n : 0);
+    double* stage = (double*)cached_stage(elems * sizeof(double));
+    if (!stage) return RANDUTV_ERR_NOMEM;
+    double* dT = stage;
+    double* dU = U ? stage + size_t(m) * n : nullptr;
+    double* dV = U ? dU + size_t(m) * m : nullptr;
     RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
                               cudaMemcpyDefault, st));
     rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb);
@@ -475,9 +494,6 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
       }
     }
     RUTV_CK(cudaStreamSynchronize(st));
-    cudaFree(dT);
-    if (dU) cudaFree(dU);
-    if (dV) cudaFree(dV);
     return rc;
   } catch (const CudaError& e) {
     fprintf(stderr, "randutv: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);
@@ -493,6 +509,31 @@ int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b
   int rc = randutv_factor_ex(&o, m, n, A, lda, b, q, seed, k_stop, U, T, V, nullptr);
   if (rc == 0 && cudaStreamSynchronize(cudaStreamPerThread) != cudaSuccess) return RANDUTV_ERR_CUDA;
   return rc;
+}
+
+long long randutv_launch_count(void) { return launches_total(); }
+
+int randutv_profile_begin(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  prof_begin();
+  return 0;
+}
+
+int randutv_profile_end(double* ms, double* flops, long long* launches) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  double m4[K_NCLASS], f4[K_NCLASS];
+  long long c4[K_NCLASS];
+  try {
+    prof_end(m4, f4, c4);
+  } catch (const CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+  for (int i = 0; i < K_NCLASS; ++i) {
+    if (ms) ms[i] = m4[i];
+    if (flops) flops[i] = f4[i];
+    if (launches) launches[i] = c4[i];
+  }
+  return 0;
 }
 
 int randutv_gaussian(double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed, uint32_t step,

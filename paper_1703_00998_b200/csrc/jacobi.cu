@@ -182,6 +182,7 @@ jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict
   // complete Vs for (numerically) zero singular values: Gram-Schmidt against e_c
   int nz = 0;
   for (int j = 0; j < k; ++j) nz += (sig[j] <= 1e-290);
+  __syncthreads();
   if (nz == 0) {
     if (threadIdx.x == 0 && sweeps_out) {
       int s = 0;
@@ -260,7 +261,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   int* counts = reinterpret_cast<int*>(work + size_t(2) * batch * k * k);
   {
     dim3 g((unsigned)std::min<int64_t>(cdiv(int64_t(k) * k, 256), 64), batch);
-    jacobi_init_k<<<g, 256, 0, st>>>(batch, k, R, ldr, strideR, Bw, Wm, counts);
+    { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_init_k<<<g, 256, 0, st>>>(batch, k, R, ldr, strideR, Bw, Wm, counts); }
     RUTV_LAUNCH_CK();
   }
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
@@ -271,12 +272,26 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   }
   const double tol = double(k) * DBL_EPSILON;
   if (k > 1) {
-    for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
-      for (int round = 0; round < d.nb - 1; ++round) {
-        dim3 g(d.nb / 2, batch);
-        jacobi_round_k<<<g, JNT, smem, st>>>(d, sweep, round, Bw, Wm, counts, tol);
-        RUTV_LAUNCH_CK();
+    // Sweeps are launched in chunks; between chunks the host reads the
+    // per-matrix rotation counts once (one sync) and stops when all converged.
+    int sweep = 0;
+    int chunk = 8;
+    std::vector<int> h(size_t(batch) * (MAX_SWEEPS + 1));
+    while (sweep < MAX_SWEEPS) {
+      int end = std::min(MAX_SWEEPS, sweep + chunk);
+      for (; sweep < end; ++sweep) {
+        for (int round = 0; round < d.nb - 1; ++round) {
+          dim3 g(d.nb / 2, batch);
+          { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_round_k<<<g, JNT, smem, st>>>(d, sweep, round, Bw, Wm, counts, tol); }
+          RUTV_LAUNCH_CK();
+        }
       }
+      RUTV_CK(cudaMemcpyAsync(h.data(), counts, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, st));
+      RUTV_CK(cudaStreamSynchronize(st));
+      bool all = true;
+      for (int b = 0; b < batch; ++b) all &= (h[size_t(b) * (MAX_SWEEPS + 1) + sweep] == 0);
+      if (all) break;
+      chunk = 2;
     }
   }
   const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
@@ -285,7 +300,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
     RUTV_CK(cudaFuncSetAttribute(jacobi_finalize_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
     attr_f = fsmem;
   }
-  jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out);
+  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out); }
   RUTV_LAUNCH_CK();
 }
 

@@ -10,6 +10,21 @@ namespace rutv {
 
 int num_sms();
 
+// ---- prof.cu: launch counting and optional per-class event timing ---------
+enum KClass { K_GEMM = 0, K_QR = 1, K_SVD = 2, K_MISC = 3, K_NCLASS = 4 };
+void count_launch(int cls, int n = 1);
+long long launches_total();
+struct ProfScope {
+  ProfScope(cudaStream_t st, int cls, double flops);
+  ~ProfScope();
+  cudaStream_t st_;
+  int cls_;
+  double flops_;
+  void* a_;
+};
+void prof_begin();
+void prof_end(double* ms, double* flops, long long* counts);
+
 // ---- gemm.cu -------------------------------------------------------------
 // C = alpha op(A) op(B) + beta C.  ``part`` (part_elems doubles) is the split-K
 // scratch; force_splits > 0 overrides the split heuristic.

@@ -97,34 +97,34 @@ dim3 grid2(int64_t m, int64_t n) {
 
 void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc) {
   if (m <= 0 || n <= 0) return;
-  scale_k<<<grid2(m, n), TB, 0, st>>>(m, n, beta, C, ldc);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); scale_k<<<grid2(m, n), TB, 0, st>>>(m, n, beta, C, ldc); }
   RUTV_LAUNCH_CK();
 }
 
 void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0 || S == D) return;
-  copy_k<<<grid2(m, n), TB, 0, st>>>(m, n, S, lds, D, ldd);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); copy_k<<<grid2(m, n), TB, 0, st>>>(m, n, S, lds, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 
 void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
-  ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 1.0);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 1.0); }
   RUTV_LAUNCH_CK();
 }
 
 void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
-  ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 0.0);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 0.0); }
   RUTV_LAUNCH_CK();
 }
 
 void copy_norm_check(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D,
                      int64_t ldd, double* scratch, double* out2, int* flag) {
   int blocks = std::min(grid_for(m * n), 4096);
-  norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag); }
   RUTV_LAUNCH_CK();
-  norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 
@@ -134,9 +134,9 @@ void fro2(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, d
     return;
   }
   int blocks = std::min(grid_for(m * n), 4096);
-  norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, nullptr, 0, scratch, nullptr);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, nullptr, 0, scratch, nullptr); }
   RUTV_LAUNCH_CK();
-  norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 
@@ -144,14 +144,14 @@ void gaussian_fill(cudaStream_t st, double* G, int64_t ldg, int64_t rows, int64_
                    uint32_t step, uint32_t purpose) {
   if (rows <= 0 || cols <= 0) return;
   int64_t total = ((rows + 1) / 2) * cols;
-  gaussian_k<<<grid_for(total), TB, 0, st>>>(G, ldg, rows, cols, uint32_t(seed & 0xffffffffu),
-                                             uint32_t(seed >> 32), step, purpose);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); gaussian_k<<<grid_for(total), TB, 0, st>>>(G, ldg, rows, cols, uint32_t(seed & 0xffffffffu),
+                                             uint32_t(seed >> 32), step, purpose); }
   RUTV_LAUNCH_CK();
 }
 
 void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, double* D, int64_t ldd) {
   if (m <= 0 || k <= 0) return;
-  diag_block_k<<<grid2(m, k), TB, 0, st>>>(m, k, d, D, ldd);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); diag_block_k<<<grid2(m, k), TB, 0, st>>>(m, k, d, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 

@@ -1,0 +1,81 @@
+// Launch accounting and optional per-kernel-class CUDA-event timing.
+// bench.py uses it to report gpu_launches and the dominant kernel's achieved
+// throughput (roofline); it is off unless randutv_profile_begin() was called.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rutv {
+
+namespace {
+std::atomic<long long> g_launches[K_NCLASS];
+struct Rec {
+  int cls;
+  cudaEvent_t a, b;
+  double flops;
+};
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_used = 0;
+
+cudaEvent_t take_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    RUTV_CK(cudaEventCreate(&e));
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+}  // namespace
+
+void count_launch(int cls, int n) { g_launches[cls].fetch_add(n, std::memory_order_relaxed); }
+
+long long launches_total() {
+  long long s = 0;
+  for (int i = 0; i < K_NCLASS; ++i) s += g_launches[i].load();
+  return s;
+}
+
+ProfScope::ProfScope(cudaStream_t st, int cls, double flops) : st_(st), cls_(cls), flops_(flops), a_(nullptr) {
+  if (!g_on) return;
+  a_ = take_event();
+  RUTV_CK(cudaEventRecord((cudaEvent_t)a_, st_));
+}
+
+ProfScope::~ProfScope() {
+  if (!g_on || !a_) return;
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, st_);
+  g_recs.push_back(Rec{cls_, (cudaEvent_t)a_, b, flops_});
+}
+
+void prof_begin() {
+  g_on = true;
+  g_recs.clear();
+  g_pool_used = 0;
+}
+
+void prof_end(double* ms, double* flops, long long* counts) {
+  RUTV_CK(cudaDeviceSynchronize());
+  for (int c = 0; c < K_NCLASS; ++c) {
+    ms[c] = 0.0;
+    flops[c] = 0.0;
+    counts[c] = 0;
+  }
+  for (auto& r : g_recs) {
+    float t = 0.f;
+    RUTV_CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    flops[r.cls] += r.flops;
+    counts[r.cls] += 1;
+  }
+  g_on = false;
+  g_recs.clear();
+  g_pool_used = 0;
+}
+
+}  // namespace rutv

@@ -246,6 +246,8 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  ProfScope _p(st, K_QR, 0.0);
+  count_launch(K_QR);
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, m, j0, wj, V, ldv, R, ldr, tau, Tw, ldt));
 }
 
@@ -275,6 +277,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
   else return ERR_UNSUPPORTED;
   const int C = (int)std::max<int64_t>(1, std::min<int64_t>(QR_MAX_CLUSTER, cdiv(m, int64_t(QR_NT) * RPT)));
   set_zero(st, b, b, Tw, ldt);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); }
   zero_lower_k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b * b, 256), 1024)), 256, 0, st>>>(b, R, ldr);
   RUTV_LAUNCH_CK();
   for (int64_t j0 = 0; j0 < b; j0 += W) {
