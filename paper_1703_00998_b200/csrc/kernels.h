@@ -31,6 +31,10 @@ void prof_end(double* ms, double* flops, long long* counts);
 void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* part,
            size_t part_elems, int force_splits = 0);
+// op(A) op(B) with the K range split: partial products at part + z*M*N (ld M),
+// z < returned split count; no reduction (the caller sums in fixed order).
+int dgemm_partials(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* part, size_t part_elems);
 int gemm_choose_splits(int64_t M, int64_t N, int64_t K, size_t part_elems);
 
 // ---- misc.cu ---------------------------------------------------------------

@@ -58,8 +58,9 @@ __device__ __forceinline__ double warp_transpose_reduce(double (&v)[W], int lane
 struct LeafSmem {
   // W <= 32
   double red[QR_WARPS][32];
-  double part[2][32];   // this CTA's partial d_k (double-buffered by column parity)
-  double rowv[2][32];   // the diagonal row's values (written by its owner CTA)
+  double part[2][QR_MAX_CLUSTER][32];  // partial d_k pushed by every CTA (double-buffered by column parity)
+  double rowv[2][32];   // the diagonal row's values (pushed by its owner CTA)
+  double rowl[32];      // owner's local copy before the push
   double tot[32];
   double rowj[32];
   double wk[32];
@@ -104,51 +105,62 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
   if (tid < 32)
     for (int k = 0; k < 33; ++k) sm.tl[tid][k] = 0.0;
 
-#pragma unroll
-  for (int j = 0; j < W; ++j) {
-    if (j >= wj) break;
+  // The column loop is NOT unrolled (an unrolled W-column body thrashed the
+  // instruction cache: ncu r01 showed 'no_instructions' as the top stall).
+  // Register arrays are indexed only by compile-time k; the runtime column j
+  // enters through selects.
+#pragma unroll 1
+  for (int j = 0; j < wj; ++j) {
     const int buf = j & 1;
     // ---- phase A: partial inner products over own rows strictly below row j
+    double x[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      double xi = 0.0;
+#pragma unroll
+      for (int k = 0; k < W; ++k) xi = (k == j) ? a[i][k] : xi;
+      x[i] = (rr[i] > j) ? xi : 0.0;
+    }
     double d[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) d[k] = 0.0;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      if (rr[i] > j) {
-        const double x = a[i][j];
+    for (int i = 0; i < RPT; ++i)
 #pragma unroll
-        for (int k = 0; k < W; ++k) d[k] = fma(x, a[i][k], d[k]);
-      }
-    }
+      for (int k = 0; k < W; ++k) d[k] = fma(x[i], a[i][k], d[k]);
     double wsum = warp_transpose_reduce<W>(d, lane);
     if (lane < W) sm.red[warp][lane] = wsum;
-    // the owner of relative row j publishes that row
+    // the owner of relative row j stages that row locally
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
       if (rr[i] == j) {
 #pragma unroll
-        for (int k = 0; k < W; ++k) sm.rowv[buf][k] = a[i][k];
+        for (int k = 0; k < W; ++k) sm.rowl[k] = a[i][k];
       }
     __syncthreads();
+    // push this CTA's partial (and, from the owner, row j) into every CTA's
+    // slots: remote stores are fire-and-forget, the reads below are local
+    const int owner = (int)(int64_t(j) / rpc);
     if (tid < W) {
       double s = 0.0;
 #pragma unroll
       for (int w2 = 0; w2 < QR_WARPS; ++w2) s += sm.red[w2][tid];
-      sm.part[buf][tid] = s;
+      const double rv = sm.rowl[tid];
+      for (int c = 0; c < C; ++c) {
+        *cluster.map_shared_rank(&sm.part[buf][crank][tid], c) = s;
+        if (crank == owner) *cluster.map_shared_rank(&sm.rowv[buf][tid], c) = rv;
+      }
     }
     cluster.sync();
     // ---- phase B: cluster-wide totals (fixed rank order -> identical on all CTAs)
-    if (tid < W) {
-      double s = 0.0;
-      for (int c = 0; c < C; ++c) s += *cluster.map_shared_rank(&sm.part[buf][tid], c);
-      const int owner = (int)(int64_t(j) / rpc);
-      sm.tot[tid] = s;
-      sm.rowj[tid] = *cluster.map_shared_rank(&sm.rowv[buf][tid], owner);
-    }
-    __syncwarp();
     if (warp == 0) {
-      double alpha = sm.rowj[j];
-      double xnorm2 = sm.tot[j];
+      double tot = 0.0, rowj = 0.0;
+      if (lane < W) {
+        for (int c = 0; c < C; ++c) tot += sm.part[buf][c][lane];
+        rowj = sm.rowv[buf][lane];
+      }
+      const double alpha = __shfl_sync(0xffffffffu, rowj, j);
+      const double xnorm2 = __shfl_sync(0xffffffffu, tot, j);
       double tau_j = 0.0, beta = alpha, scal = 0.0;
       if (xnorm2 > 0.0) {
         double nrm = sqrt(fma(alpha, alpha, xnorm2));
@@ -157,8 +169,7 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
         scal = 1.0 / (alpha - beta);
       }
       // lane k: t_k = V(:,k)^T v_j (k < j) or the update coefficient (k > j)
-      double tk = 0.0;
-      if (lane < W) tk = fma(scal, sm.tot[lane], sm.rowj[lane]);
+      const double tk = fma(scal, tot, rowj);
       if (lane < W) sm.wk[lane] = (lane > j && lane < wj) ? tau_j * tk : 0.0;
       // T(0:j, j) = -tau_j T(0:j, 0:j) t
       double tsum = 0.0;
@@ -166,7 +177,6 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
         double tc = __shfl_sync(0xffffffffu, tk, c);
         if (lane <= c) tsum = fma(sm.tl[lane][c], tc, tsum);
       }
-      __syncwarp();
       if (lane < j) sm.tl[lane][j] = -tau_j * tsum;
       if (lane == 0) {
         sm.tl[j][j] = tau_j;
@@ -176,22 +186,21 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
       }
     }
     __syncthreads();
-    // ---- phase C: apply H_j to own rows, store v_j
-    const double scal = sm.scal;
+    // ---- phase C: apply H_j to own rows (coef = v_r below row j, 1 on row j), store v_j
+    const double scal = sm.scal, beta = sm.beta;
     double wk[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) wk[k] = sm.wk[k];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      if (rr[i] > j) {
-        const double v = scal * a[i][j];
+      const double v = scal * x[i];
+      const double coef = (rr[i] > j) ? v : ((rr[i] == j) ? 1.0 : 0.0);
+      const double newj = (rr[i] > j) ? v : beta;
+      const bool setj = rr[i] >= j;
 #pragma unroll
-        for (int k = j + 1; k < W; ++k) a[i][k] = fma(-v, wk[k], a[i][k]);
-        a[i][j] = v;
-      } else if (rr[i] == j) {
-#pragma unroll
-        for (int k = j + 1; k < W; ++k) a[i][k] -= wk[k];
-        a[i][j] = sm.beta;
+      for (int k = 0; k < W; ++k) {
+        double t = fma(-coef, wk[k], a[i][k]);
+        a[i][k] = (k == j) ? (setj ? newj : a[i][k]) : t;
       }
     }
     if (crank == 0 && tid == 0) tau[j0 + j] = sm.tau;
@@ -251,6 +260,34 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, m, j0, wj, V, ldv, R, ldr, tau, Tw, ldt));
 }
 
+// O = T_l^T (sum_z part_z),  part_z = wj x b split-K partials of V_l^T V[j0:, 0:b].
+// One CTA per 32 columns; the split sum runs in fixed order (deterministic).
+__global__ void __launch_bounds__(256)
+qr_small_k(int wj, int64_t b, int splits, const double* __restrict__ part, const double* __restrict__ Tl,
+           int64_t ldt, double* __restrict__ O) {
+  __shared__ double sS[32][33];
+  __shared__ double sT[32][33];
+  const int tid = threadIdx.x;
+  const int64_t c0 = int64_t(blockIdx.x) * 32;
+  const int64_t slice = int64_t(wj) * b;
+  for (int idx = tid; idx < 32 * 32; idx += 256) {
+    int k = idx % 32, c = idx / 32;
+    double s = 0.0;
+    if (k < wj && c0 + c < b)
+      for (int z = 0; z < splits; ++z) s += part[int64_t(z) * slice + k + (c0 + c) * wj];
+    sS[k][c] = s;
+    sT[k][c] = (k < wj && c < wj) ? Tl[k + int64_t(c) * ldt] : 0.0;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 32 * 32; idx += 256) {
+    int i = idx % 32, c = idx / 32;
+    if (i >= wj || c0 + c >= b) continue;
+    double s = 0.0;
+    for (int k = 0; k <= i && k < wj; ++k) s = fma(sT[k][i], sS[k][c], s);  // T_l upper triangular
+    O[i + (c0 + c) * wj] = s;
+  }
+}
+
 // zero the strictly-lower part of the b x b R and the whole Tw before a panel
 __global__ void zero_lower_k(int64_t b, double* R, int64_t ldr) {
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < b * b; idx += int64_t(gridDim.x) * blockDim.x) {
@@ -294,20 +331,19 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     if (rest == 0 && j0 == 0) continue;
     const double* Vl = V + j0 + j0 * ldv;
     const double* Tl = Tw + j0 + j0 * ldt;
-    // S = V_l^T V[j0:, 0:b]   (wj x b)
-    dgemm(st, true, false, wj, b, rows, 1.0, Vl, ldv, V + j0, ldv, 0.0, w.sfull, wj, w.part, w.part_elems);
-    if (rest > 0) {
-      // S2 = T_l^T S(:, j0+wj:b);  V[j0:, j0+wj:b] -= V_l S2
-      dgemm(st, true, false, wj, rest, wj, 1.0, Tl, ldt, w.sfull + (j0 + wj) * wj, wj, 0.0, w.s2, wj, w.part,
-            w.part_elems);
-      dgemm(st, false, false, rows, rest, wj, -1.0, Vl, ldv, w.s2, wj, 1.0, V + j0 + (j0 + wj) * ldv, ldv, w.part,
-            w.part_elems);
+    // S = V_l^T V[j0:, 0:b] as split-K partials; O = T_l^T S  (wj x b)
+    const int splits = dgemm_partials(st, true, false, wj, b, rows, Vl, ldv, V + j0, ldv, w.part, w.part_elems);
+    {
+      ProfScope _p(st, K_QR, 0.0);
+      count_launch(K_QR);
+      qr_small_k<<<(unsigned)cdiv(b, 32), 256, 0, st>>>(wj, b, splits, w.part, Tl, ldt, w.sfull);
+      RUTV_LAUNCH_CK();
     }
-    if (j0 > 0) {
-      // Z = S(:, 0:j0)^T T_l  (j0 x wj);  Tw[0:j0, j0:j0+wj] = -Tw[0:j0, 0:j0] Z
-      dgemm(st, true, false, j0, wj, wj, 1.0, w.sfull, wj, Tl, ldt, 0.0, w.z, j0, w.part, w.part_elems);
-      dgemm(st, false, false, j0, wj, j0, -1.0, Tw, ldt, w.z, j0, 0.0, Tw + j0 * ldt, ldt, w.part, w.part_elems);
-    }
+    if (rest > 0)  // V[j0:, j0+wj:b] -= V_l O(:, j0+wj:b)
+      dgemm(st, false, false, rows, rest, wj, -1.0, Vl, ldv, w.sfull + (j0 + wj) * wj, wj, 1.0,
+            V + j0 + (j0 + wj) * ldv, ldv, w.part, w.part_elems);
+    if (j0 > 0)    // Tw[0:j0, j0:j0+wj] = -Tw[0:j0, 0:j0] O(:, 0:j0)^T
+      dgemm(st, false, true, j0, wj, j0, -1.0, Tw, ldt, w.sfull, wj, 0.0, Tw + j0 * ldt, ldt, w.part, w.part_elems);
   }
   return OK;
 }
