@@ -150,12 +150,15 @@ RANDUTV_API int randutv_small_svd_batched(int32_t batch, int32_t k, const double
 RANDUTV_API long long randutv_launch_count(void);
 
 /* Between begin and end every kernel launch is bracketed by CUDA events on its
- * stream.  end synchronises the device and returns, per kernel class
- * [0 = DMMA GEMM, 1 = panel-QR leaf, 2 = Jacobi SVD, 3 = memory-bound helpers],
- * the summed event time in ms, the summed algorithmic flops (2MNK for GEMMs,
- * 0 otherwise) and the launch count.  Arrays hold 4 entries (may be NULL). */
+ * stream.  end synchronises the device and returns, per kernel class, the
+ * summed event time in ms, the summed algorithmic flops (2MNK for GEMMs, 0
+ * otherwise) and the launch count.  Arrays hold RANDUTV_PROFILE_CLASSES
+ * entries (may be NULL); unused trailing classes are zero.  Class names:
+ * randutv_profile_class_name(i) (NULL past the last class). */
+#define RANDUTV_PROFILE_CLASSES 16
 RANDUTV_API int randutv_profile_begin(void);
 RANDUTV_API int randutv_profile_end(double* ms, double* flops, long long* launches);
+RANDUTV_API const char* randutv_profile_class_name(int cls);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,8 @@ def lib():
     L.randutv_profile_begin.restype = ctypes.c_int
     L.randutv_profile_end.argtypes = [c_vp, c_vp, c_vp]
     L.randutv_profile_end.restype = ctypes.c_int
+    L.randutv_profile_class_name.argtypes = [ctypes.c_int]
+    L.randutv_profile_class_name.restype = ctypes.c_char_p
     for f in ("randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_small_svd_batched"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -91,9 +93,7 @@ def lib():
 EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
             "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr",
             "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
-            "randutv_profile_end"]
-
-KERNEL_CLASSES = ("dmma_gemm", "panel_qr_leaf", "jacobi_svd", "memory_helpers")
+            "randutv_profile_end", "randutv_profile_class_name"]
 
 
 def launch_count() -> int:
@@ -107,11 +107,18 @@ def profile_begin():
 
 def profile_end() -> dict:
     """Per-class event time (ms), algorithmic flops and launches since profile_begin()."""
-    ms = (ctypes.c_double * 4)()
-    fl = (ctypes.c_double * 4)()
-    ln = (ctypes.c_longlong * 4)()
-    _check(lib().randutv_profile_end(ms, fl, ln), "randutv_profile_end")
-    return {k: {"ms": ms[i], "flops": fl[i], "launches": ln[i]} for i, k in enumerate(KERNEL_CLASSES)}
+    L = lib()
+    ms = (ctypes.c_double * 16)()
+    fl = (ctypes.c_double * 16)()
+    ln = (ctypes.c_longlong * 16)()
+    _check(L.randutv_profile_end(ms, fl, ln), "randutv_profile_end")
+    out = {}
+    for i in range(16):
+        name = L.randutv_profile_class_name(i)
+        if name is None:
+            break
+        out[name.decode()] = {"ms": ms[i], "flops": fl[i], "launches": ln[i]}
+    return out
 
 
 # --------------------------------------------------------------------------- layout helpers

@@ -194,6 +194,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     if (b * i < m && b * i < n) {
       const int64_t si = i - 1;  // 0-based step slot
       // ---- sketch
+      set_gemm_role(C_GEMM_SKETCH);
       gaussian_fill(st, w.G, m, mi, b, seed, uint32_t(i - 1), 0u);
       dg(w, st, true, false, ni, b, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
       double* Ycur = w.Y;
@@ -218,6 +219,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       double* Tv = w.Tv + size_t(si) * b * b;
       check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, w.qw));
       // ---- right apply to all m rows
+      set_gemm_role(C_GEMM_RIGHT);
       double* TJ = T + r0 * m;
       dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
       dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
@@ -237,6 +239,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       copy_matrix(st, b, b, R11, b, X, m);
       set_zero(st, mi - b, b, X + b, m);
       // ---- left apply to T(r0:m, J3)
+      set_gemm_role(C_GEMM_LEFT);
       const int64_t nc = n - f2;
       double* Cm = T + r0 + f2 * m;
       dg(w, st, true, false, nc, b, mi, 1.0, Cm, m, Wu, ldwu, 0.0, w.Wt, n);       // C^T W_u
@@ -271,6 +274,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   }
   if (!final_block && !stopped) k_done = std::min(k_done, n);
 
+  set_gemm_role(C_GEMM_OTHER);
   // ---- batched small SVDs
   int max_sweeps = 0;
   if (steps > 0)
@@ -523,17 +527,25 @@ int randutv_profile_end(double* ms, double* flops, long long* launches) {
   std::lock_guard<std::mutex> lock(g_mu);
   double m4[K_NCLASS], f4[K_NCLASS];
   long long c4[K_NCLASS];
+  static_assert(K_NCLASS <= 16, "profile arrays hold 16 classes");
   try {
     prof_end(m4, f4, c4);
   } catch (const CudaError&) {
     return RANDUTV_ERR_CUDA;
   }
-  for (int i = 0; i < K_NCLASS; ++i) {
-    if (ms) ms[i] = m4[i];
-    if (flops) flops[i] = f4[i];
-    if (launches) launches[i] = c4[i];
+  for (int i = 0; i < 16; ++i) {
+    if (ms) ms[i] = i < K_NCLASS ? m4[i] : 0.0;
+    if (flops) flops[i] = i < K_NCLASS ? f4[i] : 0.0;
+    if (launches) launches[i] = i < K_NCLASS ? c4[i] : 0;
   }
   return 0;
+}
+
+const char* randutv_profile_class_name(int cls) {
+  static const char* names[K_NCLASS] = {"gemm_sketch", "gemm_right_apply", "gemm_left_apply", "gemm_panel_qr",
+                                        "gemm_other",  "qr_leaf",          "qr_small",        "jacobi_svd",
+                                        "memory_helpers"};
+  return (cls >= 0 && cls < K_NCLASS) ? names[cls] : nullptr;
 }
 
 int randutv_gaussian(double* G, int64_t ldg, int64_t rows, int64_t cols, uint64_t seed, uint32_t step,

@@ -11,7 +11,19 @@ namespace rutv {
 int num_sms();
 
 // ---- prof.cu: launch counting and optional per-class event timing ---------
-enum KClass { K_GEMM = 0, K_QR = 1, K_SVD = 2, K_MISC = 3, K_NCLASS = 4 };
+// Kernel classes of the profiler.  GEMMs are attributed to the role the
+// driver is in (set_gemm_role); K_GEMM means "the current role".
+enum KClass {
+  C_GEMM_SKETCH = 0, C_GEMM_RIGHT = 1, C_GEMM_LEFT = 2, C_GEMM_QR = 3, C_GEMM_OTHER = 4,
+  C_QR_LEAF = 5, C_QR_SMALL = 6, C_SVD = 7, C_MISC = 8, K_NCLASS = 9,
+  K_GEMM = -1, K_QR = C_QR_LEAF, K_SVD = C_SVD, K_MISC = C_MISC
+};
+int set_gemm_role(int role);  // returns the previous role
+struct GemmRole {
+  int prev;
+  explicit GemmRole(int r) : prev(set_gemm_role(r)) {}
+  ~GemmRole() { set_gemm_role(prev); }
+};
 void count_launch(int cls, int n = 1);
 long long launches_total();
 struct ProfScope {

@@ -32,7 +32,19 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
-void count_launch(int cls, int n) { g_launches[cls].fetch_add(n, std::memory_order_relaxed); }
+namespace {
+int g_role = C_GEMM_OTHER;
+}
+
+int set_gemm_role(int role) {
+  int prev = g_role;
+  g_role = role;
+  return prev;
+}
+
+static inline int resolve(int cls) { return cls == K_GEMM ? g_role : cls; }
+
+void count_launch(int cls, int n) { g_launches[resolve(cls)].fetch_add(n, std::memory_order_relaxed); }
 
 long long launches_total() {
   long long s = 0;
@@ -40,7 +52,8 @@ long long launches_total() {
   return s;
 }
 
-ProfScope::ProfScope(cudaStream_t st, int cls, double flops) : st_(st), cls_(cls), flops_(flops), a_(nullptr) {
+ProfScope::ProfScope(cudaStream_t st, int cls, double flops)
+    : st_(st), cls_(resolve(cls)), flops_(flops), a_(nullptr) {
   if (!g_on) return;
   a_ = take_event();
   RUTV_CK(cudaEventRecord((cudaEvent_t)a_, st_));

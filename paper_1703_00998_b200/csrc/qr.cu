@@ -56,24 +56,57 @@ __device__ __forceinline__ double warp_transpose_reduce(double (&v)[W], int lane
 }
 
 struct LeafSmem {
-  // W <= 32
   double red[QR_WARPS][32];
-  double part[2][QR_MAX_CLUSTER][32];  // partial d_k pushed by every CTA (double-buffered by column parity)
-  double rowv[2][32];   // the diagonal row's values (pushed by its owner CTA)
-  double rowl[32];      // owner's local copy before the push
-  double tot[32];
-  double rowj[32];
-  double wk[32];
-  double tl[32][33];    // leaf T factor
-  double scal, beta, tau;
+  double part[2][QR_MAX_CLUSTER][32];  // partial d_s pushed by every CTA (double-buffered by column parity)
+  double rowv[2][32];                  // the diagonal row's values (pushed by its owner CTA)
+  double rowl[32];                     // owner's local copy before the push
+  double w[32];                        // update coefficients of the current reflector
+  double taus[32];
+  double scal, beta;
 };
 
+// Stride (doubles) of the per-CTA copy of the finished reflectors in shared
+// memory; == 4 (mod 16) so the DMMA fragment loads of the Gram are conflict free.
+template <int W>
+__host__ __device__ constexpr int vstride() { return W == 4 ? 4 : W + 4; }
+
+template <int W, int RPT>
+constexpr size_t leaf_dyn_smem() {
+  return size_t(QR_NT) * RPT * vstride<W>() * sizeof(double);
+}
+// dynamic smem: the reflector copy, reused afterwards for the Gram reduction
+// (8 warp partials + 16 cluster slots of 32x32, and the 2 x 32x33 T work area)
+template <int W, int RPT>
+constexpr size_t leaf_smem_bytes() {
+  constexpr size_t red = sizeof(double) * (size_t(QR_WARPS) * 1024 + size_t(QR_MAX_CLUSTER) * 1024);
+  return leaf_dyn_smem<W, RPT>() > red ? leaf_dyn_smem<W, RPT>() : red;
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Leaf factorization of W (<= 32) columns on a cluster of C CTAs.
+//
+// Register layout: thread t of CTA c owns relative rows rbeg_c + t + i*QR_NT
+// (i < RPT) and keeps them in a[i][s], where slot s holds leaf column j + s at
+// column step j: the reflector update writes slot s from slot s+1
+// (a <- a - coef w shifted by one), so the current column is always slot 0 and
+// no runtime register indexing or select chain is needed.  Each finished
+// column is streamed out (V explicit, R above the diagonal) and copied to
+// shared memory; the leaf T factor is formed at the end from the Gram
+// V_l^T V_l (DMMA over each CTA's rows + one cluster reduction) with the dlarft
+// recurrence T(0:j,j) = -tau_j T(0:j,0:j) (V^T v_j)(0:j).
 template <int W, int RPT>
 __global__ void __launch_bounds__(QR_NT, 1)
 leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ldv, double* __restrict__ R,
                int64_t ldr, double* __restrict__ tau, double* __restrict__ Tw, int64_t ldt) {
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ LeafSmem sm;
+  extern __shared__ __align__(16) double vsm[];  // [QR_NT*RPT rows][vstride]
+  constexpr int SV = vstride<W>();
   const int C = (int)cluster.num_blocks();
   const int crank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -81,6 +114,7 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
   const int64_t rpc = (rows + C - 1) / C;      // rows per CTA
   const int64_t rbeg = int64_t(crank) * rpc;
   const int64_t rend = min(rows, rbeg + rpc);
+  const int nloc = (int)(rend > rbeg ? rend - rbeg : 0);
 
   // rows above the leaf's diagonal block are finished R entries of these columns
   if (crank == 0) {
@@ -99,47 +133,35 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
     rr[i] = rbeg + tid + int64_t(i) * QR_NT;
     const bool ok = rr[i] < rend;
 #pragma unroll
-    for (int k = 0; k < W; ++k) a[i][k] = (ok && k < wj) ? V[(j0 + rr[i]) + (j0 + k) * ldv] : 0.0;
+    for (int s = 0; s < W; ++s) a[i][s] = (ok && s < wj) ? V[(j0 + rr[i]) + (j0 + s) * ldv] : 0.0;
     if (!ok) rr[i] = -1;
   }
-  if (tid < 32)
-    for (int k = 0; k < 33; ++k) sm.tl[tid][k] = 0.0;
 
-  // The column loop is NOT unrolled (an unrolled W-column body thrashed the
-  // instruction cache: ncu r01 showed 'no_instructions' as the top stall).
-  // Register arrays are indexed only by compile-time k; the runtime column j
-  // enters through selects.
+  // dots for column 0: d_s = sum_{r > 0} a_{r,0} a_{r,s}
+  double d[W];
+#pragma unroll
+  for (int s = 0; s < W; ++s) d[s] = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const double x = (rr[i] > 0) ? a[i][0] : 0.0;
+#pragma unroll
+    for (int s = 0; s < W; ++s) d[s] = fma(x, a[i][s], d[s]);
+  }
+
 #pragma unroll 1
   for (int j = 0; j < wj; ++j) {
     const int buf = j & 1;
-    // ---- phase A: partial inner products over own rows strictly below row j
-    double x[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      double xi = 0.0;
-#pragma unroll
-      for (int k = 0; k < W; ++k) xi = (k == j) ? a[i][k] : xi;
-      x[i] = (rr[i] > j) ? xi : 0.0;
-    }
-    double d[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) d[k] = 0.0;
-#pragma unroll
-    for (int i = 0; i < RPT; ++i)
-#pragma unroll
-      for (int k = 0; k < W; ++k) d[k] = fma(x[i], a[i][k], d[k]);
+    // ---- reduce d over the CTA (warp transpose-reduce, then across warps)
     double wsum = warp_transpose_reduce<W>(d, lane);
     if (lane < W) sm.red[warp][lane] = wsum;
-    // the owner of relative row j stages that row locally
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
       if (rr[i] == j) {
 #pragma unroll
-        for (int k = 0; k < W; ++k) sm.rowl[k] = a[i][k];
+        for (int s = 0; s < W; ++s) sm.rowl[s] = a[i][s];
       }
     __syncthreads();
-    // push this CTA's partial (and, from the owner, row j) into every CTA's
-    // slots: remote stores are fire-and-forget, the reads below are local
+    // ---- push this CTA's partial (and, from the owner, row j) into every CTA
     const int owner = (int)(int64_t(j) / rpc);
     if (tid < W) {
       double s = 0.0;
@@ -152,86 +174,156 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
       }
     }
     cluster.sync();
-    // ---- phase B: cluster-wide totals (fixed rank order -> identical on all CTAs)
+    // ---- scalars of H_j (every CTA, same fixed-order sums -> identical values)
     if (warp == 0) {
       double tot = 0.0, rowj = 0.0;
       if (lane < W) {
-        for (int c = 0; c < C; ++c) tot += sm.part[buf][c][lane];
+        double pv[QR_MAX_CLUSTER];
+#pragma unroll
+        for (int c = 0; c < QR_MAX_CLUSTER; ++c) pv[c] = (c < C) ? sm.part[buf][c][lane] : 0.0;
+#pragma unroll
+        for (int c = 0; c < QR_MAX_CLUSTER; ++c) tot += pv[c];
         rowj = sm.rowv[buf][lane];
       }
-      const double alpha = __shfl_sync(0xffffffffu, rowj, j);
-      const double xnorm2 = __shfl_sync(0xffffffffu, tot, j);
+      const double alpha = __shfl_sync(0xffffffffu, rowj, 0);
+      const double xnorm2 = __shfl_sync(0xffffffffu, tot, 0);
       double tau_j = 0.0, beta = alpha, scal = 0.0;
       if (xnorm2 > 0.0) {
-        double nrm = sqrt(fma(alpha, alpha, xnorm2));
+        const double nrm = sqrt(fma(alpha, alpha, xnorm2));
         beta = -copysign(nrm, alpha);
         tau_j = (beta - alpha) / beta;
         scal = 1.0 / (alpha - beta);
       }
-      // lane k: t_k = V(:,k)^T v_j (k < j) or the update coefficient (k > j)
-      const double tk = fma(scal, tot, rowj);
-      if (lane < W) sm.wk[lane] = (lane > j && lane < wj) ? tau_j * tk : 0.0;
-      // T(0:j, j) = -tau_j T(0:j, 0:j) t
-      double tsum = 0.0;
-      for (int c = 0; c < j; ++c) {
-        double tc = __shfl_sync(0xffffffffu, tk, c);
-        if (lane <= c) tsum = fma(sm.tl[lane][c], tc, tsum);
-      }
-      if (lane < j) sm.tl[lane][j] = -tau_j * tsum;
+      // slot s >= 1 (column j+s): w_s = tau_j v_j^T a_{:,j+s}
+      if (lane < W) sm.w[lane] = (lane >= 1 && j + lane < wj) ? tau_j * fma(scal, tot, rowj) : 0.0;
       if (lane == 0) {
-        sm.tl[j][j] = tau_j;
+        sm.taus[j] = tau_j;
         sm.scal = scal;
         sm.beta = beta;
-        sm.tau = tau_j;
       }
     }
     __syncthreads();
-    // ---- phase C: apply H_j to own rows (coef = v_r below row j, 1 on row j), store v_j
+    // ---- apply H_j to own rows (shifting slots by one), emit column j,
+    //      and accumulate the dots of column j+1
     const double scal = sm.scal, beta = sm.beta;
-    double wk[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) wk[k] = sm.wk[k];
+    double coef[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const double v = scal * x[i];
-      const double coef = (rr[i] > j) ? v : ((rr[i] == j) ? 1.0 : 0.0);
-      const double newj = (rr[i] > j) ? v : beta;
-      const bool setj = rr[i] >= j;
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        double t = fma(-coef, wk[k], a[i][k]);
-        a[i][k] = (k == j) ? (setj ? newj : a[i][k]) : t;
-      }
-    }
-    if (crank == 0 && tid == 0) tau[j0 + j] = sm.tau;
-  }
-  // ---- write back: V explicit (unit lower trapezoidal), R upper
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    if (rr[i] < 0) continue;
-    const int64_t r = rr[i], gr = j0 + r;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      if (k >= wj) break;
-      double* vp = V + gr + (j0 + k) * ldv;
-      if (r < k) {
-        R[gr + (j0 + k) * ldr] = a[i][k];
-        *vp = 0.0;
-      } else if (r == k) {
-        R[gr + (j0 + k) * ldr] = a[i][k];
-        *vp = 1.0;
+      coef[i] = 0.0;
+      if (rr[i] < 0) continue;
+      const int64_t r = rr[i];
+      const double xj = a[i][0];
+      const double v = scal * xj;
+      coef[i] = (r > j) ? v : ((r == j) ? 1.0 : 0.0);
+      double* vp = V + (j0 + r) + (j0 + j) * ldv;
+      if (r <= j) {
+        R[(j0 + r) + (j0 + j) * ldr] = (r == j) ? beta : xj;
+        *vp = (r == j) ? 1.0 : 0.0;
       } else {
-        *vp = a[i][k];
+        *vp = v;
+      }
+      vsm[(tid + i * QR_NT) * SV + j] = (r > j) ? v : ((r == j) ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < W - 1; ++s) {
+      const double ws = sm.w[s + 1];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) a[i][s] = fma(-coef[i], ws, a[i][s + 1]);
+    }
+#pragma unroll
+    for (int s = 0; s < W; ++s) d[s] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      a[i][W - 1] = 0.0;
+      const double x = (rr[i] > j + 1) ? a[i][0] : 0.0;
+#pragma unroll
+      for (int s = 0; s < W - 1; ++s) d[s] = fma(x, a[i][s], d[s]);
+    }
+  }
+
+  // ---- leaf T factor from the Gram G = V_l^T V_l of the stored reflectors
+  // zero the unused columns of the local copy (wj < W) and rows beyond nloc
+  for (int idx = tid; idx < QR_NT * RPT; idx += QR_NT) {
+    for (int c = wj; c < W; ++c) vsm[idx * SV + c] = 0.0;
+    if (idx >= nloc)
+      for (int c = 0; c < wj; ++c) vsm[idx * SV + c] = 0.0;
+  }
+  __syncthreads();
+  constexpr int NTL = (W + 7) / 8;  // 8x8 tiles per dimension
+  double g[NTL][NTL][2];
+#pragma unroll
+  for (int p = 0; p < NTL; ++p)
+#pragma unroll
+    for (int q = 0; q < NTL; ++q) g[p][q][0] = g[p][q][1] = 0.0;
+  {
+    const int gq = lane >> 2, tq = lane & 3;
+    const int nslot = QR_NT * RPT;            // local rows (padded with zeros)
+    const int per_warp = nslot / QR_WARPS;    // multiple of 4
+    for (int k0 = warp * per_warp; k0 < (warp + 1) * per_warp; k0 += 4) {
+      const double* rowp = vsm + (k0 + tq) * SV;
+      double af[NTL];
+#pragma unroll
+      for (int p = 0; p < NTL; ++p) af[p] = (p * 8 + gq < W) ? rowp[p * 8 + gq] : 0.0;
+#pragma unroll
+      for (int p = 0; p < NTL; ++p)
+#pragma unroll
+        for (int q = 0; q < NTL; ++q) dmma884(g[p][q], af[p], af[q]);
+    }
+  }
+  __syncthreads();  // every warp is done with vsm: reuse it for the reduction
+  double* gw = vsm;                                 // [QR_WARPS][32*32]
+  {
+    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int p = 0; p < NTL; ++p)
+#pragma unroll
+      for (int q = 0; q < NTL; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = p * 8 + gq, col = q * 8 + 2 * tq + e;
+          gw[warp * 1024 + row * 32 + col] = g[p][q][e];
+        }
+  }
+  __syncthreads();
+  cluster.sync();  // rank 0's reduction area (its vsm tail) is free of readers
+  double* slots = vsm + QR_WARPS * 1024;           // rank 0: [C][32*32]
+  for (int idx = tid; idx < W * W; idx += QR_NT) {
+    const int row = idx / W, col = idx % W;
+    double s = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < QR_WARPS; ++w2) s += gw[w2 * 1024 + row * 32 + col];
+    *cluster.map_shared_rank(&slots[crank * 1024 + row * 32 + col], 0) = s;
+  }
+  cluster.sync();
+  if (crank == 0) {
+    double* G = gw;  // [32][33] reuse
+    for (int idx = tid; idx < W * W; idx += QR_NT) {
+      const int row = idx / W, col = idx % W;
+      double s = 0.0;
+      for (int c = 0; c < C; ++c) s += slots[c * 1024 + row * 32 + col];
+      G[row * 33 + col] = s;
+    }
+    __syncthreads();
+    // T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j); T stored over G's upper triangle
+    double* Tm = gw + 32 * 33;  // [32][33]
+    if (warp == 0) {
+      for (int j = 0; j < wj; ++j) {
+        const double tau_j = sm.taus[j];
+        double s = 0.0;
+        if (lane < j)
+          for (int c = lane; c < j; ++c) s = fma(Tm[lane * 33 + c], G[c * 33 + j], s);
+        __syncwarp();
+        if (lane < 32) Tm[lane * 33 + j] = (lane < j) ? -tau_j * s : (lane == j ? tau_j : 0.0);
+        __syncwarp();
       }
     }
-  }
-  if (crank == 0) {
+    __syncthreads();
     for (int idx = tid; idx < wj * wj; idx += QR_NT) {
-      int r = idx % wj, k = idx / wj;
-      Tw[(j0 + r) + (j0 + k) * ldt] = (r <= k) ? sm.tl[r][k] : 0.0;
+      const int r = idx % wj, k = idx / wj;
+      Tw[(j0 + r) + (j0 + k) * ldt] = (r <= k) ? Tm[r * 33 + k] : 0.0;
     }
+    for (int j = tid; j < wj; j += QR_NT) tau[j0 + j] = sm.taus[j];
   }
-  cluster.sync();  // keep DSMEM alive until every CTA is done reading
 }
 
 template <int W, int RPT>
@@ -241,12 +333,13 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
   auto kern = leaf_qr_kernel<W, RPT>;
   if (!attr) {
     RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaf_smem_bytes<W, RPT>()));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(QR_NT, 1, 1);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = leaf_smem_bytes<W, RPT>();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -260,31 +353,53 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, m, j0, wj, V, ldv, R, ldr, tau, Tw, ldt));
 }
 
-// O = T_l^T (sum_z part_z),  part_z = wj x b split-K partials of V_l^T V[j0:, 0:b].
-// One CTA per 32 columns; the split sum runs in fixed order (deterministic).
+// O = T_l^T S, S = sum_z part_z with part_z the b x wj split-K partials of
+// S^T = V[j0:, 0:b]^T V_l (ld b).  4 columns of S per CTA; the split sum is
+// spread over 8 thread groups and combined in fixed order (deterministic).
 __global__ void __launch_bounds__(256)
 qr_small_k(int wj, int64_t b, int splits, const double* __restrict__ part, const double* __restrict__ Tl,
            int64_t ldt, double* __restrict__ O) {
-  __shared__ double sS[32][33];
+  __shared__ double sS[32][5];
   __shared__ double sT[32][33];
+  __shared__ double red[8][4 * 32 + 1];
   const int tid = threadIdx.x;
-  const int64_t c0 = int64_t(blockIdx.x) * 32;
+  const int64_t c0 = int64_t(blockIdx.x) * 4;  // 4 columns (of S) per CTA
   const int64_t slice = int64_t(wj) * b;
+  {
+    // thread (g = tid / 32, e = tid % 32): element (c = e % 4 + ..) -- lanes map
+    // to (column c0 + e/8 .. ) pairs so that loads of one split are contiguous
+    const int g = tid >> 5, e = tid & 31;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (e < wj) {
+      for (int z = g; z < splits; z += 8) {
+        const double* pz = part + int64_t(z) * slice + int64_t(e) * b + c0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c0 + c < b) acc[c] += pz[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[g][c * 32 + e] = acc[c];
+  }
   for (int idx = tid; idx < 32 * 32; idx += 256) {
     int k = idx % 32, c = idx / 32;
-    double s = 0.0;
-    if (k < wj && c0 + c < b)
-      for (int z = 0; z < splits; ++z) s += part[int64_t(z) * slice + k + (c0 + c) * wj];
-    sS[k][c] = s;
     sT[k][c] = (k < wj && c < wj) ? Tl[k + int64_t(c) * ldt] : 0.0;
   }
   __syncthreads();
-  for (int idx = tid; idx < 32 * 32; idx += 256) {
-    int i = idx % 32, c = idx / 32;
-    if (i >= wj || c0 + c >= b) continue;
+  if (tid < 128) {
     double s = 0.0;
-    for (int k = 0; k <= i && k < wj; ++k) s = fma(sT[k][i], sS[k][c], s);  // T_l upper triangular
-    O[i + (c0 + c) * wj] = s;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) s += red[g][tid];
+    sS[tid % 32][tid / 32] = s;
+  }
+  __syncthreads();
+  if (tid < 128) {
+    int i = tid % 32, c = tid / 32;
+    if (i < wj && c0 + c < b) {
+      double s = 0.0;
+      for (int k = 0; k <= i; ++k) s = fma(sT[k][i], sS[k][c], s);  // T_l upper triangular
+      O[i + (c0 + c) * wj] = s;
+    }
   }
 }
 
@@ -305,6 +420,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
              double* Tw, int64_t ldt, const QrWork& w) {
   if (b <= 0) return OK;
   if (m < b) return ERR_UNSUPPORTED;
+  GemmRole role(C_GEMM_QR);
   int W, RPT;
   const int64_t cap = int64_t(QR_MAX_CLUSTER) * QR_NT;
   if (m <= cap * 2) { W = 32; RPT = 2; }
@@ -331,12 +447,12 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     if (rest == 0 && j0 == 0) continue;
     const double* Vl = V + j0 + j0 * ldv;
     const double* Tl = Tw + j0 + j0 * ldt;
-    // S = V_l^T V[j0:, 0:b] as split-K partials; O = T_l^T S  (wj x b)
-    const int splits = dgemm_partials(st, true, false, wj, b, rows, Vl, ldv, V + j0, ldv, w.part, w.part_elems);
+    // S^T = V[j0:, 0:b]^T V_l (b x wj, skinny tile) as split-K partials; O = T_l^T S  (wj x b)
+    const int splits = dgemm_partials(st, true, false, b, wj, rows, V + j0, ldv, Vl, ldv, w.part, w.part_elems);
     {
-      ProfScope _p(st, K_QR, 0.0);
-      count_launch(K_QR);
-      qr_small_k<<<(unsigned)cdiv(b, 32), 256, 0, st>>>(wj, b, splits, w.part, Tl, ldt, w.sfull);
+      ProfScope _p(st, C_QR_SMALL, 0.0);
+      count_launch(C_QR_SMALL);
+      qr_small_k<<<(unsigned)cdiv(b, 4), 256, 0, st>>>(wj, b, splits, w.part, Tl, ldt, w.sfull);
       RUTV_LAUNCH_CK();
     }
     if (rest > 0)  // V[j0:, j0+wj:b] -= V_l O(:, j0+wj:b)
@@ -350,6 +466,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
 
 void thin_q(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const double* Tw, int64_t ldt,
             double* Q, int64_t ldq, double* tmp_bb, double* part, size_t part_elems) {
+  GemmRole role(C_GEMM_QR);
   // tmp = Tw V1^T (V1 = V[0:b, 0:b]);  Q = E - V tmp
   dgemm(st, false, true, b, b, b, 1.0, Tw, ldt, V, ldv, 0.0, tmp_bb, b, part, part_elems);
   set_identity(st, m, b, Q, ldq);
