@@ -44,7 +44,7 @@ extern "C" {
 #define RANDUTV_ERR_NCCL 4        /* reserved for the multi-GPU path                  */
 #define RANDUTV_ERR_UNSUPPORTED 5 /* shape outside this build (e.g. > 65536 rows)    */
 
-#define RANDUTV_MAX_B 1024
+#define RANDUTV_MAX_B 512
 
 /* Options of randutv_factor_ex.  Zero-initialise, then set what you need. */
 typedef struct randutv_opts {

@@ -11,6 +11,7 @@
 // A sweep with no rotation (|gamma| <= tol sqrt(alpha beta), tol = k eps)
 // marks the matrix converged and later launches exit immediately.
 #include <cfloat>
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -18,10 +19,12 @@
 #include <algorithm>
 #include <vector>
 
+namespace cg = cooperative_groups;
+
 namespace rutv {
 
 namespace {
-constexpr int JNT = 256;
+constexpr int JNT = 512;
 constexpr int MAX_SWEEPS = 40;
 
 struct JacobiDesc {
@@ -61,11 +64,134 @@ __device__ __forceinline__ void rr_pair(int nplayers, int round, int i, int& p, 
   }
 }
 
-// One block-pair operation for tournament round ``round`` of sweep ``sweep``.
+// One cyclic sweep over all column pairs of a block pair held in shared
+// memory (sB, sW: ncol columns of length k <= 32*EPL), one warp per pair and
+// round.  Each lane keeps its EPL elements of the two columns in registers
+// (fully unrolled: the loads, the dot product and the W loads are issued
+// back to back).  Column norms are computed once and then tracked with
+// Rutishauser's exact update (alpha' = alpha - t gamma, beta' = beta + t
+// gamma), so a pair costs a single warp reduction.  Returns this warp's
+// rotation count.
+template <int EPL>
+__device__ int pair_sweep(double* sB, double* sW, double* nrm, int k, int ncol, int kb, int bp, int bq, double tol) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto valid = [&](int c) { return ((c < kb) ? bp * kb + c : bq * kb + (c - kb)) < k; };
+  for (int c = warp; c < ncol; c += nw) {
+    const double* x = sB + size_t(c) * k;
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const int r = lane + 32 * e;
+      const double v = (r < k) ? x[r] : 0.0;
+      s = fma(v, v, s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm[c] = s;
+  }
+  __syncthreads();
+  int rotations = 0;
+  for (int rnd = 0; rnd < ncol - 1; ++rnd) {
+    for (int pi = warp; pi < ncol / 2; pi += nw) {
+      int p, q;
+      rr_pair(ncol, rnd, pi, p, q);
+      if (!valid(p) || !valid(q)) continue;
+      double* bp_ = sB + size_t(p) * k;
+      double* bq_ = sB + size_t(q) * k;
+      double x[EPL], y[EPL];
+      double ga = 0.0;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const int r = lane + 32 * e;
+        x[e] = (r < k) ? bp_[r] : 0.0;
+        y[e] = (r < k) ? bq_[r] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) ga = fma(x[e], y[e], ga);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      const double al = nrm[p], be = nrm[q];
+      if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+        double* wp = sW + size_t(p) * k;
+        double* wq = sW + size_t(q) * k;
+        constexpr int EPW = EPL <= 8 ? EPL : 1;  // W elements preloaded (register budget at 512 threads)
+        double u[EPW], v[EPW];
+        if constexpr (EPL <= 8) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            const int r = lane + 32 * e;
+            u[e] = (r < k) ? wp[r] : 0.0;
+            v[e] = (r < k) ? wq[r] : 0.0;
+          }
+        }
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (fabs(zeta) > 1e150) ? 0.5 / zeta
+                                              : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double c = rsqrt(fma(t, t, 1.0));
+        const double s = c * t;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const int r = lane + 32 * e;
+          if (r < k) {
+            bp_[r] = c * x[e] - s * y[e];
+            bq_[r] = s * x[e] + c * y[e];
+            const double uu = (EPL <= 8) ? u[e < EPW ? e : 0] : wp[r];
+            const double vv = (EPL <= 8) ? v[e < EPW ? e : 0] : wq[r];
+            wp[r] = c * uu - s * vv;
+            wq[r] = s * uu + c * vv;
+          }
+        }
+        if (lane == 0) {
+          nrm[p] = al - t * ga;
+          nrm[q] = be + t * ga;
+          ++rotations;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return rotations;
+}
+
+__device__ __forceinline__ int pair_sweep_any(double* sB, double* sW, double* nrm, int k, int ncol, int kb, int bp,
+                                              int bq, double tol) {
+  if (k <= 32) return pair_sweep<1>(sB, sW, nrm, k, ncol, kb, bp, bq, tol);
+  if (k <= 64) return pair_sweep<2>(sB, sW, nrm, k, ncol, kb, bp, bq, tol);
+  if (k <= 128) return pair_sweep<4>(sB, sW, nrm, k, ncol, kb, bp, bq, tol);
+  if (k <= 256) return pair_sweep<8>(sB, sW, nrm, k, ncol, kb, bp, bq, tol);
+  return pair_sweep<16>(sB, sW, nrm, k, ncol, kb, bp, bq, tol);  // k <= 512 (larger k: see jacobi_svd_batched)
+}
+
+__device__ void load_pair(double* sB, double* sW, const double* B, const double* W, int k, int kb, int bp, int bq) {
+  const int ncol = 2 * kb;
+  for (int idx = threadIdx.x; idx < ncol * k; idx += blockDim.x) {
+    int c = idx / k, r = idx % k;
+    int g = (c < kb) ? bp * kb + c : bq * kb + (c - kb);
+    bool ok = g < k;
+    sB[idx] = ok ? __ldcg(B + r + int64_t(g) * k) : 0.0;
+    sW[idx] = ok ? __ldcg(W + r + int64_t(g) * k) : 0.0;
+  }
+}
+
+__device__ void store_pair(const double* sB, const double* sW, double* B, double* W, int k, int kb, int bp, int bq) {
+  const int ncol = 2 * kb;
+  for (int idx = threadIdx.x; idx < ncol * k; idx += blockDim.x) {
+    int c = idx / k, r = idx % k;
+    int g = (c < kb) ? bp * kb + c : bq * kb + (c - kb);
+    if (g < k) {
+      __stcg(B + r + int64_t(g) * k, sB[idx]);
+      __stcg(W + r + int64_t(g) * k, sW[idx]);
+    }
+  }
+}
+
+// One block-pair operation for tournament round ``round`` of sweep ``sweep``
+// (one launch per round; used when a matrix's blocks do not fit one cluster).
 __global__ void __launch_bounds__(JNT)
 jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ Bw, double* __restrict__ Wm,
                int* __restrict__ counts, double tol) {
   extern __shared__ __align__(16) double js[];
+  __shared__ double nrm[64];
   const int mat = blockIdx.y;
   int* cnt = counts + mat * (MAX_SWEEPS + 1);
   if (cnt[sweep] == 0) return;  // previous sweep did no rotation: converged
@@ -74,71 +200,56 @@ jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ Bw, doub
   rr_pair(d.nb, round, blockIdx.x, bp, bq);
   double* B = Bw + int64_t(mat) * k * k;
   double* W = Wm + int64_t(mat) * k * k;
-  const int ncol = 2 * kb;
-  double* sB = js;                     // [ncol][k]
-  double* sW = js + size_t(ncol) * k;  // [ncol][k]
-  // column c of the pair -> global column
-  auto gcol = [&](int c) { return (c < kb) ? bp * kb + c : bq * kb + (c - kb); };
-  for (int idx = threadIdx.x; idx < ncol * k; idx += JNT) {
-    int c = idx / k, r = idx % k;
-    int g = gcol(c);
-    bool ok = g < k;
-    sB[idx] = ok ? B[r + int64_t(g) * k] : 0.0;
-    sW[idx] = ok ? W[r + int64_t(g) * k] : 0.0;
-  }
+  double* sB = js;
+  double* sW = js + size_t(2 * kb) * k;
+  load_pair(sB, sW, B, W, k, kb, bp, bq);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int rotations = 0;
-  for (int rnd = 0; rnd < ncol - 1; ++rnd) {
-    for (int pi = warp; pi < kb; pi += JNT / 32) {
-      int p, q;
-      rr_pair(ncol, rnd, pi, p, q);
-      if (gcol(p) >= k || gcol(q) >= k) continue;
-      double* bp_ = sB + size_t(p) * k;
-      double* bq_ = sB + size_t(q) * k;
-      double al = 0.0, be = 0.0, ga = 0.0;
-      for (int r = lane; r < k; r += 32) {
-        double x = bp_[r], y = bq_[r];
-        al = fma(x, x, al);
-        be = fma(y, y, be);
-        ga = fma(x, y, ga);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        al += __shfl_xor_sync(0xffffffffu, al, o);
-        be += __shfl_xor_sync(0xffffffffu, be, o);
-        ga += __shfl_xor_sync(0xffffffffu, ga, o);
-      }
-      if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-        double zeta = (be - al) / (2.0 * ga);
-        double t = (fabs(zeta) > 1e150) ? 0.5 / zeta
-                                        : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        double c = 1.0 / sqrt(fma(t, t, 1.0));
-        double s = c * t;
-        double* wp = sW + size_t(p) * k;
-        double* wq = sW + size_t(q) * k;
-        for (int r = lane; r < k; r += 32) {
-          double x = bp_[r], y = bq_[r];
-          bp_[r] = c * x - s * y;
-          bq_[r] = s * x + c * y;
-          double u = wp[r], v = wq[r];
-          wp[r] = c * u - s * v;
-          wq[r] = s * u + c * v;
-        }
-        if (lane == 0) ++rotations;
-      }
-    }
+  int rot = pair_sweep_any(sB, sW, nrm, k, 2 * kb, kb, bp, bq, tol);
+  store_pair(sB, sW, B, W, k, kb, bp, bq);
+  if ((threadIdx.x & 31) == 0 && rot) atomicAdd(&cnt[sweep + 1], rot);
+}
+
+// Whole Jacobi SVD of one matrix per cluster (nb/2 CTAs, one block pair
+// each): the tournament rounds and the sweeps run inside the kernel, with a
+// cluster barrier between rounds (columns move between CTAs through L2) and a
+// cluster-wide rotation count deciding convergence.
+__global__ void __launch_bounds__(JNT)
+jacobi_cluster_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts,
+                 double tol) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double js[];
+  __shared__ double nrm[64];
+  __shared__ int rot_sm;
+  const int mat = blockIdx.y;
+  const int cta = (int)cluster.block_rank();
+  int* cnt = counts + mat * (MAX_SWEEPS + 1);
+  const int k = d.k, kb = d.kb;
+  double* B = Bw + int64_t(mat) * k * k;
+  double* W = Wm + int64_t(mat) * k * k;
+  double* sB = js;
+  double* sW = js + size_t(2 * kb) * k;
+  for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+    if (threadIdx.x == 0) rot_sm = 0;
     __syncthreads();
-  }
-  for (int idx = threadIdx.x; idx < ncol * k; idx += JNT) {
-    int c = idx / k, r = idx % k;
-    int g = gcol(c);
-    if (g < k) {
-      B[r + int64_t(g) * k] = sB[idx];
-      W[r + int64_t(g) * k] = sW[idx];
+    int rot = 0;
+    for (int round = 0; round < d.nb - 1; ++round) {
+      int bp, bq;
+      rr_pair(d.nb, round, cta, bp, bq);
+      load_pair(sB, sW, B, W, k, kb, bp, bq);
+      __syncthreads();
+      rot += pair_sweep_any(sB, sW, nrm, k, 2 * kb, kb, bp, bq, tol);
+      store_pair(sB, sW, B, W, k, kb, bp, bq);
+      __threadfence();
+      cluster.sync();
     }
+    if ((threadIdx.x & 31) == 0 && rot) atomicAdd(&rot_sm, rot);
+    __syncthreads();
+    if (threadIdx.x == 0 && rot_sm) atomicAdd(&cnt[sweep + 1], rot_sm);
+    __threadfence();
+    cluster.sync();
+    const int total = atomicAdd(&cnt[sweep + 1], 0);
+    if (total == 0) break;
   }
-  if (lane == 0 && rotations) atomicAdd(&cnt[sweep + 1], rotations);
 }
 
 // sigma_j = ||B(:,j)||, sort descending, Us = W(:,perm), Vs = B(:,perm)/sigma.
@@ -265,13 +376,36 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
     RUTV_LAUNCH_CK();
   }
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
-  static size_t attr_smem = 0;
-  if (smem > 48 * 1024 && smem > attr_smem) {
-    RUTV_CK(cudaFuncSetAttribute(jacobi_round_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_smem = smem;
-  }
   const double tol = double(k) * DBL_EPSILON;
-  if (k > 1) {
+  const int csize = d.nb / 2;
+  if (k > 1 && csize <= 8) {
+    // one cluster per matrix runs every round and sweep in-kernel
+    static size_t attr_c = 0;
+    if (smem > attr_c) {
+      RUTV_CK(cudaFuncSetAttribute(jacobi_cluster_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_c = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize, batch, 1);
+    cfg.blockDim = dim3(JNT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope _p(st, K_SVD, 0.0);
+    count_launch(K_SVD);
+    RUTV_CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_k, d, Bw, Wm, counts, tol));
+  } else if (k > 1) {
+    static size_t attr_smem = 0;
+    if (smem > 48 * 1024 && smem > attr_smem) {
+      RUTV_CK(cudaFuncSetAttribute(jacobi_round_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_smem = smem;
+    }
     // Sweeps are launched in chunks; between chunks the host reads the
     // per-matrix rotation counts once (one sync) and stops when all converged.
     int sweep = 0;
