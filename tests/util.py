@@ -14,7 +14,7 @@ def ek_fro(T: np.ndarray) -> np.ndarray:
 
 
 def parity_floor(n: int, a_fro: float, c: float = 1.0) -> float:
-    """Absolute rounding floor F = c n eps ||A||_F of the parity rule (R13)."""
+    """Absolute rounding floor F = c n eps ||A||_F of the parity rule (R18)."""
     return c * n * EPS * a_fro
 
 
