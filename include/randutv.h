@@ -52,7 +52,9 @@ typedef struct randutv_opts {
   double tol;             /* > 0: stop after a step once ||T(I3,J3)||_F <= tol ||A||_F       */
   int32_t no_reortho;     /* 0 (default): re-orthonormalise Y before every X Y in the power
                              loop (R5); 1: plain power loop      */
-  int32_t reserved0;
+  int32_t qr_mode;        /* 0 (default): panel QRs by CholeskyQR2 + Householder
+                             reconstruction, column-by-column Householder as the fallback
+                             for ill-conditioned panels (R20); 1: Householder only */
   void* workspace;        /* optional caller device workspace (NULL: library cache)        */
   size_t workspace_bytes; /* its size; must be >= randutv_workspace_size(...)              */
 } randutv_opts;
@@ -63,7 +65,8 @@ typedef struct randutv_info {
   int32_t steps;        /* randomised steps taken (the ``if`` branch of P:939)           */
   int32_t final_block;  /* 1 if the final SVD block (``else`` branch) ran         */
   int32_t max_sweeps;   /* most Jacobi sweeps any small SVD needed                       */
-  int32_t reserved0;
+  int32_t qr_fallbacks; /* panel QRs / re-orthonormalisations that took the Householder
+                           fallback (qr_mode 0)                                           */
   double trailing_fro;  /* ||T(k_done+1:m, k_done+1:n)||_F (0 for a full factorisation)  */
   double a_fro;         /* ||A||_F                                                        */
 } randutv_info;
@@ -96,8 +99,9 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
 
 /* As randutv_factor, with options and diagnostics.  Device pointers are
  * processed asynchronously on opts->stream, except that the call synchronises
- * that stream once after validating A (non-finite scan) and once per step when
- * opts->tol > 0 (early-stop test).  Returns after all work is enqueued; with
+ * that stream once after validating A (non-finite scan), once per step when
+ * opts->tol > 0 (early-stop test) and once per panel QR / re-orthonormalisation
+ * in qr_mode 0 (the CholeskyQR2 fallback decision).  Returns after all work is enqueued; with
  * host buffers it returns after completion. */
 RANDUTV_API int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
                       int32_t q, uint64_t seed, int64_t k_stop, double* U, double* T, double* V,
@@ -134,6 +138,15 @@ RANDUTV_API int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t
  * ldt) the forward compact-WY factor: H_1...H_b = I - V Tw V^T. */
 RANDUTV_API int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
                      double* Tw, int64_t ldt, void* stream);
+
+/* randutv_panel_qr with the algorithm chosen: mode 0 = CholeskyQR2 of the panel
+ * followed by the Householder reconstruction of Ballard et al. (same V, R, tau,
+ * Tw in exact arithmetic; R20), falling back to mode 1 when the panel
+ * is too ill-conditioned (then *fallback = 1, else 0; fallback may be NULL);
+ * mode 1 = column-by-column Householder (cluster leaf kernel + DMMA updates).
+ * Synchronises ``stream`` once in mode 0 (the fallback decision).  10 mode. */
+RANDUTV_API int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                        double* Tw, int64_t ldt, int32_t mode, int32_t* fallback, void* stream);
 
 /* Batched SVD of ``batch`` k x k matrices: R_i at R + i*strideR
  * (ld ldr) = Us_i diag(D_i) Vs_i^T, D_i >= 0 non-increasing.  D is batch x k,

@@ -35,13 +35,13 @@ class RandUTVError(RuntimeError):
 
 
 class _Opts(ctypes.Structure):
-    _fields_ = [("stream", c_vp), ("tol", c_dbl), ("no_reortho", c_i32), ("reserved0", c_i32),
+    _fields_ = [("stream", c_vp), ("tol", c_dbl), ("no_reortho", c_i32), ("qr_mode", c_i32),
                 ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t)]
 
 
 class _Info(ctypes.Structure):
     _fields_ = [("k_done", c_i64), ("steps", c_i32), ("final_block", c_i32), ("max_sweeps", c_i32),
-                ("reserved0", c_i32), ("trailing_fro", c_dbl), ("a_fro", c_dbl)]
+                ("qr_fallbacks", c_i32), ("trailing_fro", c_dbl), ("a_fro", c_dbl)]
 
 
 @dataclass
@@ -52,6 +52,7 @@ class Info:
     max_sweeps: int
     trailing_fro: float
     a_fro: float
+    qr_fallbacks: int = 0
 
 
 def lib():
@@ -77,6 +78,8 @@ def lib():
     L.randutv_dgemm.argtypes = [c_i32, c_i32, c_i64, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp, c_i64, c_dbl, c_vp,
                                 c_i64, c_vp]
     L.randutv_panel_qr.argtypes = [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]
+    L.randutv_panel_qr_ex.argtypes = [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_i32,
+                                      ctypes.POINTER(c_i32), c_vp]
     L.randutv_small_svd_batched.argtypes = [c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]
     L.randutv_launch_count.restype = ctypes.c_longlong
     L.randutv_profile_begin.restype = ctypes.c_int
@@ -84,14 +87,15 @@ def lib():
     L.randutv_profile_end.restype = ctypes.c_int
     L.randutv_profile_class_name.argtypes = [ctypes.c_int]
     L.randutv_profile_class_name.restype = ctypes.c_char_p
-    for f in ("randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_small_svd_batched"):
+    for f in ("randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
+              "randutv_small_svd_batched"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
 
 
 EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
-            "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr",
+            "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
             "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
             "randutv_profile_end", "randutv_profile_class_name"]
 
@@ -163,7 +167,7 @@ def _check(rc: int, where: str):
 
 # --------------------------------------------------------------------------- the factorization
 def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reortho: bool = True,
-            with_uv: bool = True, stream=None, out=None):
+            with_uv: bool = True, stream=None, out=None, qr_mode: int = 0):
     """A = U T V^T (Fig. fig:randUTV) on the GPU.
 
     ``A``: torch CUDA tensor (m x n, m >= n) or a numpy array (host buffers,
@@ -173,7 +177,7 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
     """
     L = lib()
     if isinstance(A, np.ndarray):
-        return _randutv_host(A, b, q, seed, k_stop, tol, reortho, with_uv)
+        return _randutv_host(A, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode)
     torch = _torch()
     A = as_colmajor(A)
     m, n = A.shape
@@ -183,7 +187,8 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
         T = empty_cm(m, n, A.device)
         U = empty_cm(m, m, A.device) if with_uv else None
         V = empty_cm(n, n, A.device) if with_uv else None
-    opts = _Opts(stream=_stream(stream, A.device).value, tol=float(tol), no_reortho=0 if reortho else 1)
+    opts = _Opts(stream=_stream(stream, A.device).value, tol=float(tol), no_reortho=0 if reortho else 1,
+                 qr_mode=int(qr_mode))
     info = _Info()
     rc = L.randutv_factor_ex(ctypes.byref(opts), m, n, A.data_ptr(), _ld(A), int(b), int(q), int(seed) & (2**64 - 1),
                              int(k_stop), U.data_ptr() if U is not None else None, T.data_ptr(),
@@ -191,24 +196,24 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
     _check(rc, "randutv_factor_ex")
     del torch
     return U, T, V, Info(info.k_done, info.steps, bool(info.final_block), info.max_sweeps, info.trailing_fro,
-                         info.a_fro)
+                         info.a_fro, info.qr_fallbacks)
 
 
-def _randutv_host(A: np.ndarray, b, q, seed, k_stop, tol, reortho, with_uv):
+def _randutv_host(A: np.ndarray, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode=0):
     L = lib()
     A = np.asfortranarray(A, dtype=np.float64)
     m, n = A.shape
     T = np.empty((m, n), order="F")
     U = np.empty((m, m), order="F") if with_uv else None
     V = np.empty((n, n), order="F") if with_uv else None
-    opts = _Opts(stream=None, tol=float(tol), no_reortho=0 if reortho else 1)
+    opts = _Opts(stream=None, tol=float(tol), no_reortho=0 if reortho else 1, qr_mode=int(qr_mode))
     info = _Info()
     p = lambda X: X.ctypes.data if X is not None else None  # noqa: E731
     rc = L.randutv_factor_ex(ctypes.byref(opts), m, n, p(A), m, int(b), int(q), int(seed) & (2**64 - 1),
                              int(k_stop), p(U), p(T), p(V), ctypes.byref(info))
     _check(rc, "randutv_factor_ex(host)")
     return U, T, V, Info(info.k_done, info.steps, bool(info.final_block), info.max_sweeps, info.trailing_fro,
-                         info.a_fro)
+                         info.a_fro, info.qr_fallbacks)
 
 
 def factor_raw(m, n, A_ptr, lda, b, q, seed, k_stop, U_ptr, T_ptr, V_ptr) -> int:
@@ -241,9 +246,11 @@ def dgemm(transa: bool, transb: bool, alpha: float, A, B, beta: float, C, stream
     return C
 
 
-def panel_qr(P, stream=None):
+def panel_qr(P, stream=None, mode: int = 0, return_fallback: bool = False):
     """Householder QR of an m x b panel (copied).  Returns (V, R, tau, Tw) with
-    H_1...H_b = I - V Tw V^T and P = (I - V Tw V^T)[:, :b] R."""
+    H_1...H_b = I - V Tw V^T and P = (I - V Tw V^T)[:, :b] R.  mode 0:
+    CholeskyQR2 + Householder reconstruction (Householder fallback); mode 1:
+    column-by-column Householder.  return_fallback adds whether the fallback ran."""
     torch = _torch()
     m, b = P.shape
     V = empty_cm(m, b, P.device)
@@ -251,8 +258,12 @@ def panel_qr(P, stream=None):
     R = empty_cm(b, b, P.device)
     Tw = empty_cm(b, b, P.device)
     tau = torch.empty(b, dtype=torch.float64, device=P.device)
-    _check(lib().randutv_panel_qr(m, b, V.data_ptr(), _ld(V), R.data_ptr(), _ld(R), tau.data_ptr(), Tw.data_ptr(),
-                                  _ld(Tw), _stream(stream)), "randutv_panel_qr")
+    fb = c_i32(0)
+    _check(lib().randutv_panel_qr_ex(m, b, V.data_ptr(), _ld(V), R.data_ptr(), _ld(R), tau.data_ptr(),
+                                     Tw.data_ptr(), _ld(Tw), int(mode), ctypes.byref(fb), _stream(stream)),
+           "randutv_panel_qr_ex")
+    if return_fallback:
+        return V, R, tau, Tw, bool(fb.value)
     return V, R, tau, Tw
 
 

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_randutv.so")
-SOURCES = ["gemm.cu", "misc.cu", "qr.cu", "jacobi.cu", "prof.cu", "driver.cu"]
+SOURCES = ["gemm.cu", "misc.cu", "qr.cu", "smallmat.cu", "jacobi.cu", "prof.cu", "driver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr"]

@@ -118,6 +118,9 @@ Work carve(Arena& ar, const Plan& p) {
   w.qw.sfull = ar.take<double>(size_t(32) * b);
   w.qw.s2 = ar.take<double>(size_t(32) * b);
   w.qw.z = ar.take<double>(size_t(32) * b);
+  w.qw.q1_elems = size_t(mx) * b;
+  w.qw.q1 = ar.take<double>(w.qw.q1_elems);
+  w.qw.small = ar.take<double>(small_work_elems(b));
   w.nrm = ar.take<double>(8192);
   w.scal = ar.take<double>(16);
   w.flag = ar.take<int>(16);
@@ -167,6 +170,9 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   ar.base = (char*)ws;
   ar.size = ws_bytes;
   Work w = carve(ar, p);
+  int fallbacks = 0;
+  w.qw.mode = o.qr_mode;
+  w.qw.fallbacks = &fallbacks;
 
   // ---- T <- A, ||A||_F, non-finite scan (one host sync)
   RUTV_CK(cudaMemsetAsync(w.flag, 0, sizeof(int), st));
@@ -201,8 +207,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       double* Yalt = w.Y2;
       for (int it = 0; it < q; ++it) {
         if (reortho) {
-          check_qr(panel_qr(st, ni, b, Ycur, n, w.Rtmp, b, w.tau, w.Ttmp, b, w.qw));
-          thin_q(st, ni, b, Ycur, n, w.Ttmp, b, Yalt, n, w.Rtmp, w.part, w.part_elems);
+          check_qr(rutv::reortho(st, ni, b, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, w.qw));
           std::swap(Ycur, Yalt);
         }
         dg(w, st, false, false, mi, b, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);       // Z = X Y
@@ -372,6 +377,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       RUTV_CK(cudaStreamSynchronize(st));
       info->trailing_fro = 0.0;
     }
+    info->qr_fallbacks = fallbacks;
     info->max_sweeps = 0;
     for (int v : sw) info->max_sweeps = std::max(info->max_sweeps, v);
   }
@@ -463,6 +469,7 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
   randutv_opts o{};
   if (opts) o = *opts;
   if (o.tol < 0 || std::isnan(o.tol)) return -12;
+  if (o.qr_mode < 0 || o.qr_mode > 1) return -12;
   if (b > n) b = n;  // a single final-SVD step, same result as any b >= n
   std::lock_guard<std::mutex> lock(g_mu);
   try {
@@ -584,25 +591,40 @@ int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t 
   return 0;
 }
 
-int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
-                     double* Tw, int64_t ldt, void* stream) {
+int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                        double* Tw, int64_t ldt, int32_t mode, int32_t* fallback, void* stream) {
   if (b < 1 || b > RANDUTV_MAX_B) return -2;
   if (m < b) return -1;
   if (!V || ldv < m) return -4;
   if (!R || ldr < b) return -6;
   if (!tau) return -7;
   if (!Tw || ldt < b) return -9;
+  if (mode < 0 || mode > 1) return -10;
   std::lock_guard<std::mutex> lock(g_mu);
   try {
     size_t part = size_t(8) * m * b + size_t(148) * 32 * 1024;
     size_t extra = size_t(3) * 32 * b + 1024;
-    double* ws = (double*)cached_ws((part + extra) * sizeof(double));
+    size_t q1 = size_t(m) * b, sm = small_work_elems(b) + 64;
+    double* ws = (double*)cached_ws((part + extra + q1 + sm) * sizeof(double));
     if (!ws) return RANDUTV_ERR_NOMEM;
     QrWork w{ws, part, ws + part, ws + part + 32 * b, ws + part + 64 * b};
-    return panel_qr(stream ? (cudaStream_t)stream : cudaStreamPerThread, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
+    w.q1 = ws + part + extra;
+    w.q1_elems = q1;
+    w.small = (double*)(((uintptr_t)(w.q1 + q1) + 255) & ~uintptr_t(255));
+    w.mode = mode;
+    int fb = 0;
+    w.fallbacks = &fb;
+    int rc = panel_qr(stream ? (cudaStream_t)stream : cudaStreamPerThread, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
+    if (fallback) *fallback = fb;
+    return rc;
   } catch (const CudaError&) {
     return RANDUTV_ERR_CUDA;
   }
+}
+
+int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                     double* Tw, int64_t ldt, void* stream) {
+  return randutv_panel_qr_ex(m, b, V, ldv, R, ldr, tau, Tw, ldt, 0, nullptr, stream);
 }
 
 int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,

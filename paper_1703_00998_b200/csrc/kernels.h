@@ -68,6 +68,26 @@ void gaussian_fill(cudaStream_t st, double* G, int64_t ldg, int64_t rows, int64_
 // [k, m) of the same columns are zeroed.
 void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, double* D, int64_t ldd);
 
+// ---- smallmat.cu: b x b cluster kernels of the CholeskyQR2 panel QR --------
+struct SmallWork {
+  int bp;  // b padded to a multiple of 32; every matrix below is bp x bp, ld bp
+  double *W1, *R1, *R1i, *W2, *R2, *R2i, *F, *Li, *Ui, *M, *US;
+  double* S;      // bp signs
+  double* stats;  // [bad, min diag R1, max diag R1]
+  int* flag;      // 0: reconstruction valid
+};
+int small_pad(int64_t b);
+size_t small_work_elems(int64_t b);
+SmallWork carve_small(double* base, int64_t b);
+// W1 (Gram, b x b valid) -> R1, R1i = R1^-1; stats.
+void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w);
+// W2 = Q1^T Q1 -> second pass + Householder reconstruction: writes R (b x b,
+// ld ldr), tau, Tw (ld ldt), w.M = R2^-1 U~^-1 and w.F (L strictly below), w.flag.
+void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt);
+// V(0:b, 0:b) <- unit lower L from w.F
+void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv);
+
 // ---- qr.cu -----------------------------------------------------------------
 struct QrWork {
   double* part;      // split-K scratch for the inner GEMMs
@@ -75,8 +95,19 @@ struct QrWork {
   double* sfull;     // b_leaf x b   (V_l^T [V_prev | V_l | A_rest])
   double* s2;        // b_leaf x b
   double* z;         // b x b_leaf
+  double* q1 = nullptr;  // m x b scratch of the CholeskyQR2 path (capacity q1_elems)
+  size_t q1_elems = 0;
+  double* small = nullptr;  // small_work_elems(b) doubles
+  int mode = 0;             // 0: CholeskyQR2 + reconstruction, Householder fallback; 1: Householder only
+  int* fallbacks = nullptr; // host counter of fallbacks taken (may be null)
 };
 size_t qr_work_elems(int64_t b);
+// Q = thin orthonormal basis of span(Y) with Y = Q R, R upper triangular (the
+// re-orthonormalisation of the power loop, R5): CholeskyQR when the
+// Gram is well conditioned, Householder (panel_qr + thin_q) otherwise.  Y may
+// be overwritten.
+int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, double* Q, int64_t ldq, double* tmp_bb,
+            double* Tmp_bb, double* tau, const QrWork& w);
 // Householder QR of the m x b panel held in V (ld ldv), in place:
 // on exit V is the explicit unit-lower-trapezoidal reflector matrix, R (b x b,
 // ld ldr) the upper-triangular factor (zeros below), tau[b] the reflector

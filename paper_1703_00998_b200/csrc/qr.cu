@@ -416,10 +416,9 @@ int qr_max_rows() { return QR_MAX_CLUSTER * QR_NT * 16; }
 
 size_t qr_work_elems(int64_t b) { return size_t(3) * 32 * size_t(b) + 1024; }
 
-int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
-             double* Tw, int64_t ldt, const QrWork& w) {
-  if (b <= 0) return OK;
-  if (m < b) return ERR_UNSUPPORTED;
+namespace {
+int panel_qr_hh(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                double* Tw, int64_t ldt, const QrWork& w) {
   GemmRole role(C_GEMM_QR);
   int W, RPT;
   const int64_t cap = int64_t(QR_MAX_CLUSTER) * QR_NT;
@@ -461,6 +460,76 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     if (j0 > 0)    // Tw[0:j0, j0:j0+wj] = -Tw[0:j0, 0:j0] O(:, 0:j0)^T
       dgemm(st, false, true, j0, wj, j0, -1.0, Tw, ldt, w.sfull, wj, 0.0, Tw + j0 * ldt, ldt, w.part, w.part_elems);
   }
+  return OK;
+}
+
+int read_flag_sync(cudaStream_t st, const int* dflag) {
+  int h = 0;
+  RUTV_CK(cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RUTV_CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+void read_stats_sync(cudaStream_t st, const double* dstats, double (&h)[3]) {
+  RUTV_CK(cudaMemcpyAsync(h, dstats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RUTV_CK(cudaStreamSynchronize(st));
+}
+
+bool cholqr_ok(const QrWork& w, int64_t m, int64_t b) {
+  return w.mode == 0 && w.q1 && w.small && size_t(m) * b <= w.q1_elems && b <= 512;
+}
+}  // namespace
+
+// Householder QR of an m x b panel (see kernels.h).  Default path: CholeskyQR2
+// + Householder reconstruction (smallmat.cu, R20) -- four GEMMs over
+// the panel and two cluster kernels -- with the column-by-column Householder
+// kernel as the fallback when the panel is too ill-conditioned for CholeskyQR2
+// (Cholesky breakdown or ||Q1^T Q1 - I||_max > 1/2, i.e. kappa >~ 1e7).
+int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+             double* Tw, int64_t ldt, const QrWork& w) {
+  if (b <= 0) return OK;
+  if (m < b) return ERR_UNSUPPORTED;
+  if (cholqr_ok(w, m, b)) {
+    GemmRole role(C_GEMM_QR);
+    SmallWork sw = carve_small(w.small, b);
+    const int bp = sw.bp;
+    dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems);        // G1
+    small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
+    dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems);     // Q1
+    dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems);      // G2
+    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt);
+    if (read_flag_sync(st, sw.flag) == 0) {
+      if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
+        dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems);
+      small_put_unit_lower(st, b, sw, V, ldv);
+      return OK;
+    }
+    if (w.fallbacks) ++*w.fallbacks;
+  }
+  return panel_qr_hh(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
+}
+
+int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, double* Q, int64_t ldq, double* tmp_bb,
+            double* Tmp_bb, double* tau, const QrWork& w) {
+  if (cholqr_ok(w, m, b)) {
+    GemmRole role(C_GEMM_QR);
+    SmallWork sw = carve_small(w.small, b);
+    const int bp = sw.bp;
+    dgemm(st, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, bp, w.part, w.part_elems);
+    small_chol_inv(st, b, sw);
+    double h[3];
+    read_stats_sync(st, sw.stats, h);
+    // kappa(R1) estimated by its diagonal: CholeskyQR's loss of orthogonality
+    // ~ kappa^2 eps stays <= 1e-8 -- ample for a basis of the power loop
+    if (h[0] == 0.0 && h[2] <= 1e4 * h[1]) {
+      dgemm(st, false, false, m, b, b, 1.0, Y, ldy, sw.R1i, bp, 0.0, Q, ldq, w.part, w.part_elems);
+      return OK;
+    }
+    if (w.fallbacks) ++*w.fallbacks;
+  }
+  int rc = panel_qr_hh(st, m, b, Y, ldy, tmp_bb, b, tau, Tmp_bb, b, w);
+  if (rc != OK) return rc;
+  thin_q(st, m, b, Y, ldy, Tmp_bb, b, Q, ldq, tmp_bb, w.part, w.part_elems);
   return OK;
 }
 

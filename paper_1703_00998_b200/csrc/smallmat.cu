@@ -1,0 +1,767 @@
+// b x b kernels of the GEMM-based panel QR (qr.cu, R20):
+//
+//   CholeskyQR2 of a tall panel A (m x b):  G1 = A^T A = R1^T R1,
+//   Q1 = A R1^-1,  G2 = Q1^T Q1 = R2^T R2,  Q = Q1 R2^-1,  R = R2 R1,
+// followed by the Householder reconstruction of Ballard et al. ("Reconstructing
+// Householder vectors from tall-skinny QR", 2015): with S = diag(+-1) chosen
+// column by column so that every pivot has modulus >= 1,
+//   S - Q(0:b,:) = L U~   (LU without pivoting, L unit lower, U~ upper),
+//   W = [L; -Q(b:m,:) U~^-1],  T_w = U~ S L^-T,  R_h = S R,  tau_j = (T_w)_jj,
+// which are, in exact arithmetic, exactly the reflectors, compact-WY factor,
+// tau and R of LAPACK's Householder QR (dlarfg sign convention, R3)
+// -- the convention is fixed by the uniqueness of A = (I - W T W^T)[R_h; 0]
+// with W unit lower trapezoidal and 1 <= tau_j <= 2.
+//
+// The b x b factorizations run on ONE thread-block cluster of SC CTAs: the
+// matrices live in global memory (L2-resident, <= 2 MB), split in 32 x 32
+// tiles; every block step factors the 32 x 32 diagonal tile in registers of one
+// warp (redundantly in every CTA, so no broadcast is needed), then the CTAs
+// share the row/column-panel and trailing-update tiles (DMMA m8n8k4 on shared
+// memory tiles) with a cluster barrier between phases.  The matrices are
+// padded to bp = 32*ceil(b/32) with identity (Grams) or zeros (Q block), which
+// leaves the b x b results unchanged.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+// phase timestamps for tools/small_prof.cu (compiled out in the library)
+#ifndef SMALL_MARK
+#define SMALL_MARK(id)
+#endif
+
+namespace rutv {
+
+namespace {
+constexpr int TS = 32;    // tile size
+constexpr int SLD = 36;   // smem tile stride (== 4 mod 16 doubles: conflict-free DMMA fragments)
+constexpr int SNT = 256;  // threads per CTA
+constexpr int SC = 8;     // CTAs per cluster
+constexpr int TSZ = TS * SLD;
+
+struct SmallSm {
+  double a[TSZ], b[TSZ], c[TSZ];    // operand / intermediate tiles
+  double d[TSZ], di[TSZ], dit[TSZ];  // diagonal factor, its inverse (L^-1 for LU), transposed inverse
+  double e[TSZ];                     // U~^-1 of the diagonal tile (LU)
+  double aug[TS * 97];               // row-major augmented elimination work area [32][96] (+1 pad)
+  double piv[TS];
+  double sgn[TS];
+  double dmin, dmax;
+  int bad;
+};
+
+struct TRef {
+  const double* p;  // stored tile's (0,0) element
+  int ld;
+  int tr;           // op(X) = tr ? stored^T : stored
+};
+
+__device__ __forceinline__ const double* tile_ptr(const double* M, int ld, int i, int j) {
+  return M + i * TS + size_t(j) * TS * ld;
+}
+__device__ __forceinline__ double* tile_ptr(double* M, int ld, int i, int j) {
+  return M + i * TS + size_t(j) * TS * ld;
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cluster_barrier(cg::cluster_group& cl) {
+  __threadfence();
+  cl.sync();
+}
+
+// 32x32 tile global -> registers (4 elements per thread; L2 only, the data
+// was written by other CTAs of the cluster)
+__device__ __forceinline__ void tile_ld(double (&v)[4], const TRef& t) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+    v[u] = __ldcg(t.p + r + size_t(c) * t.ld);
+  }
+}
+// registers -> shared tile holding op(X) column-major (stride SLD)
+__device__ __forceinline__ void tile_st(double* s, const double (&v)[4], int tr) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+    if (tr) s[r * SLD + c] = v[u];
+    else s[c * SLD + r] = v[u];
+  }
+}
+__device__ __forceinline__ void tile_load_sync(double* s, const TRef& t) {
+  double v[4];
+  tile_ld(v, t);
+  tile_st(s, v, t.tr);
+  __syncthreads();
+}
+
+// acc += sA * sB (32x32x32; warp w owns rows 8(w&3).., columns 16(w>>2)..)
+__device__ __forceinline__ void tile_mma(double (&acc)[2][2], const double* sA, const double* sB) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int fr = (w & 3) * 8, fc = (w >> 2) * 16;
+#pragma unroll
+  for (int k4 = 0; k4 < 8; ++k4) {
+    const double a = sA[(k4 * 4 + t) * SLD + fr + g];
+    const double b0 = sB[(fc + g) * SLD + k4 * 4 + t];
+    const double b1 = sB[(fc + 8 + g) * SLD + k4 * 4 + t];
+    dmma(acc[0], a, b0);
+    dmma(acc[1], a, b1);
+  }
+}
+
+__device__ __forceinline__ void acc_zero(double (&acc)[2][2]) {
+  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+}
+
+// visit the accumulator elements: f(row, col, value) in tile coordinates
+template <class F>
+__device__ __forceinline__ void acc_each(const double (&acc)[2][2], F f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int fr = (w & 3) * 8, fc = (w >> 2) * 16;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) f(fr + g, fc + 8 * j + 2 * t + e, acc[j][e]);
+}
+
+__device__ __forceinline__ void acc_to_smem(const double (&acc)[2][2], double* s) {
+  acc_each(acc, [&](int r, int c, double v) { s[c * SLD + r] = v; });
+  __syncthreads();
+}
+__device__ __forceinline__ void acc_to_global(const double (&acc)[2][2], double* g, int ld, double scale) {
+  acc_each(acc, [&](int r, int c, double v) { g[r + size_t(c) * ld] = scale * v; });
+}
+
+// g(tile) -= acc, with every load issued before the first store (the
+// compiler cannot hoist loads over possibly-aliasing stores itself)
+__device__ __forceinline__ void acc_sub_global(const double (&acc)[2][2], double* g, int ld) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gg = lane >> 2, t = lane & 3;
+  const int fr = (w & 3) * 8, fc = (w >> 2) * 16;
+  double old[2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) old[j][e] = __ldcg(g + (fr + gg) + size_t(fc + 8 * j + 2 * t + e) * ld);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) g[(fr + gg) + size_t(fc + 8 * j + 2 * t + e) * ld] = old[j][e] - acc[j][e];
+}
+
+// acc = sum_{q < np} op(A_q) op(B_q), operands streamed through s.a / s.b with
+// a one-deep register prefetch.
+template <class GP>
+__device__ void tile_sum(double (&acc)[2][2], int np, GP gp, SmallSm& s) {
+  acc_zero(acc);
+  if (np <= 0) return;
+  double va[4], vb[4];
+  TRef A, B;
+  gp(0, A, B);
+  tile_ld(va, A);
+  tile_ld(vb, B);
+  for (int q = 0; q < np; ++q) {
+    __syncthreads();
+    tile_st(s.a, va, A.tr);
+    tile_st(s.b, vb, B.tr);
+    __syncthreads();
+    if (q + 1 < np) {
+      gp(q + 1, A, B);
+      tile_ld(va, A);
+      tile_ld(vb, B);
+    }
+    tile_mma(acc, s.a, s.b);
+  }
+  __syncthreads();
+}
+
+// ---- 32x32 diagonal-tile kernels, whole CTA, one barrier per column ---------
+// (Measured on B200: the per-column chain -- pivot, reciprocal, update,
+// barrier -- costs ~0.3 us; variants with one warp, shifted registers or
+// per-thread 8x8 blocks were slower because the FP64 issue rate of one warp
+// (~2.4 cycles per DFMA) or redundant per-warp work dominates.)
+//
+// Cholesky + inverse by elimination on the augmented [G | I] (row-major, ld 65):
+// after the 32 column steps the left block holds U = Dg L^T (G = L Dg L^T) and
+// the right block L^-1, so R = Dg^{1/2} L^T and R^-1 = L^-T Dg^{-1/2}.
+// In: G tile (column-major in s.d, upper triangle read).  Out: s.d = R (zeros
+// below), s.di = R^-1, s.dit = R^-T.  Non-positive / non-finite pivots of valid
+// columns set s.bad (and are replaced by 1).
+__device__ __noinline__ void cta_chol_inv(SmallSm& s, int gcol0, int b) {
+  constexpr int LD = 65;
+  double* A = s.aug;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < TS * 64; e += SNT) {
+    const int i = e >> 6, j = e & 63;
+    A[i * LD + j] = (j < TS) ? s.d[max(i, j) * SLD + min(i, j)] : ((j - TS == i) ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k < TS; ++k) {
+    double p = A[k * LD + k];
+    if (!(p > 0.0) || !isfinite(p)) p = 1.0;  // flagged below from the stored pivot
+    const double invp = 1.0 / p;
+    const double* rowk = A + k * LD;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * SNT, i = e >> 6, j = e & 63;
+      if (i > k && j > k) A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
+    }
+    __syncthreads();
+  }
+  if (tid < TS) {
+    double p = A[tid * LD + tid];
+    const bool ok = (p > 0.0) && isfinite(p);
+    if (!ok) p = 1.0;
+    const double d = sqrt(p);
+    s.piv[tid] = d;
+    s.c[tid] = 1.0 / d;
+    if (gcol0 + tid < b && !ok) atomicOr(&s.bad, 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double mn = s.dmin, mx = s.dmax;
+    for (int k = 0; k < TS && gcol0 + k < b; ++k) {
+      mn = fmin(mn, s.piv[k]);
+      mx = fmax(mx, s.piv[k]);
+    }
+    s.dmin = mn;
+    s.dmax = mx;
+  }
+  const double* rd = s.c;
+  for (int e = tid; e < TS * TS; e += SNT) {
+    const int i = e & 31, j = e >> 5;  // (row i, col j), column-major outputs
+    s.d[j * SLD + i] = (i <= j) ? A[i * LD + j] * rd[i] : 0.0;
+    const double ri = (i <= j) ? A[j * LD + TS + i] * rd[j] : 0.0;  // R^-1(i,j) = L^-1(j,i)/d_j
+    s.di[j * SLD + i] = ri;
+    s.dit[i * SLD + j] = ri;
+  }
+  __syncthreads();
+}
+
+// Sign-modified LU (Householder reconstruction: when column k becomes the
+// pivot, s_k = (a_kk <= 0 ? -1 : +1) is added, |pivot| = |a_kk| + 1 >= 1) by
+// elimination on [F | I | I] (row-major, ld 97): the middle block becomes L^-1;
+// the right block runs the forward elimination of U~^T with the rows of U~ as
+// they become final, giving E' with E' U~^T = diag(piv), so U~^-1 = E'^T diag(piv)^-1.
+// In: F tile (column-major in s.d).  Out: s.d = L (strict lower) \ U~, s.di =
+// L^-1, s.e = U~^-1, s.sgn.
+__device__ __noinline__ void cta_lu_sign_inv(SmallSm& s) {
+  constexpr int LD = 97;
+  double* A = s.aug;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < TS * 96; e += SNT) {
+    const int i = e / 96, j = e - i * 96;
+    A[i * LD + j] = (j < TS) ? s.d[j * SLD + i] : (((j - TS) & 31) == i ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k < TS; ++k) {
+    const double a = A[k * LD + k];
+    const double sg = (a <= 0.0) ? -1.0 : 1.0;
+    const double pv = a + sg;
+    const double invp = 1.0 / pv;
+    if (tid == 0) {
+      s.sgn[k] = sg;
+      s.piv[k] = pv;
+    }
+    const double* rowk = A + k * LD;
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int e = tid + u * SNT, i = e / 96, j = e - i * 96;
+      if (i <= k) continue;
+      if (j < TS) {
+        if (j > k) A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
+      } else if (j < 2 * TS) {
+        A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
+      } else {
+        A[i * LD + j] = fma(-rowk[i] * invp, rowk[j], A[i * LD + j]);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < TS) s.c[tid] = 1.0 / s.piv[tid];
+  __syncthreads();
+  const double* rp = s.c;
+  for (int e = tid; e < TS * TS; e += SNT) {
+    const int i = e & 31, j = e >> 5;
+    const double pj = s.piv[j];
+    s.d[j * SLD + i] = (i > j) ? A[i * LD + j] * rp[j] : ((i == j) ? pj : A[i * LD + j]);
+    s.di[j * SLD + i] = (i >= j) ? A[i * LD + TS + j] : 0.0;
+    s.e[j * SLD + i] = (i <= j) ? A[j * LD + 2 * TS + i] * rp[j] : 0.0;
+  }
+  __syncthreads();
+}
+
+struct SmallDims {
+  int b, bp, nb;
+};
+
+__device__ __forceinline__ void copy_tile_smem_to_global(const double* s, double* g, int ld) {
+  for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+    const int r = e & 31, c = e >> 5;
+    g[r + size_t(c) * ld] = s[c * SLD + r];
+  }
+}
+
+
+// decode the q-th upper-triangular tile (i, j), lo <= i <= j < nb
+__device__ __forceinline__ void upper_pair(int q, int lo, int nb, int& i, int& j) {
+  i = lo;
+  while (q >= nb - i) {
+    q -= nb - i;
+    ++i;
+  }
+  j = i + q;
+}
+
+// Blocked right-looking Cholesky with the inverse of the factor built along:
+// W (bp x bp, updated in place) = R^T R;  R, Ri = R^-1 (upper, zero lower tiles
+// written by the caller's init).  Stats into s.bad / s.dmin / s.dmax.
+__device__ void chol_inv_dev(cg::cluster_group& cl, const SmallDims& d, double* W, double* R, double* Ri,
+                             SmallSm& s) {
+  const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+  const int bp = d.bp, nb = d.nb;
+  for (int p = 0; p < nb; ++p) {
+    SMALL_MARK(0);
+    tile_load_sync(s.d, TRef{tile_ptr(W, bp, p, p), bp, 0});
+    SMALL_MARK(1);
+    cta_chol_inv(s, p * TS, d.b);
+    SMALL_MARK(2);
+    if (cta == 0) {
+      copy_tile_smem_to_global(s.d, tile_ptr(R, bp, p, p), bp);
+      copy_tile_smem_to_global(s.di, tile_ptr(Ri, bp, p, p), bp);
+    }
+    // phase A: R(p, j) = D^-T W(p, j) (j > p);  Ri(k, p) = -(sum_l Ri(k,l) R(l,p)) D^-1 (k < p)
+    const int nrow = nb - 1 - p;
+    for (int task = cta; task < nb - 1; task += C) {
+      double acc[2][2];
+      if (task < nrow) {
+        const int j = p + 1 + task;
+        tile_load_sync(s.a, TRef{tile_ptr(W, bp, p, j), bp, 0});
+        acc_zero(acc);
+        tile_mma(acc, s.dit, s.a);
+        acc_to_global(acc, tile_ptr(R, bp, p, j), bp, 1.0);
+      } else {
+        const int k = task - nrow;
+        tile_sum(acc, p - k, [&](int q, TRef& A, TRef& B) {
+          const int l = k + q;
+          A = TRef{tile_ptr(Ri, bp, k, l), bp, 0};
+          B = TRef{tile_ptr(R, bp, l, p), bp, 0};
+        }, s);
+        acc_to_smem(acc, s.c);
+        acc_zero(acc);
+        tile_mma(acc, s.c, s.di);
+        acc_to_global(acc, tile_ptr(Ri, bp, k, p), bp, -1.0);
+      }
+      __syncthreads();
+    }
+    SMALL_MARK(3);
+    cluster_barrier(cl);
+    SMALL_MARK(4);
+    // phase B: W(i, j) -= R(p, i)^T R(p, j), p < i <= j
+    const int nt = nrow * (nrow + 1) / 2;
+    for (int task = cta; task < nt; task += C) {
+      int i, j;
+      upper_pair(task, p + 1, nb, i, j);
+      double acc[2][2];
+      SMALL_MARK(7);
+      tile_sum(acc, 1, [&](int, TRef& A, TRef& B) {
+        A = TRef{tile_ptr(R, bp, p, i), bp, 1};
+        B = TRef{tile_ptr(R, bp, p, j), bp, 0};
+      }, s);
+      SMALL_MARK(8);
+      acc_sub_global(acc, tile_ptr(W, bp, i, j), bp);
+      __syncthreads();
+      SMALL_MARK(9);
+    }
+    SMALL_MARK(5);
+    cluster_barrier(cl);
+  }
+}
+
+// Blocked right-looking sign-modified LU of F (in place: L \ U~), with
+// Li = L^-1 and Ui = U~^-1 built along, and the signs into S (bp).
+__device__ void lu_sign_inv_dev(cg::cluster_group& cl, const SmallDims& d, double* F, double* Li, double* Ui,
+                                double* S, SmallSm& s) {
+  const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+  const int bp = d.bp, nb = d.nb;
+  for (int p = 0; p < nb; ++p) {
+    tile_load_sync(s.d, TRef{tile_ptr(F, bp, p, p), bp, 0});
+    cta_lu_sign_inv(s);
+    if (cta == 0) {
+      copy_tile_smem_to_global(s.d, tile_ptr(F, bp, p, p), bp);
+      copy_tile_smem_to_global(s.di, tile_ptr(Li, bp, p, p), bp);
+      copy_tile_smem_to_global(s.e, tile_ptr(Ui, bp, p, p), bp);
+      if (threadIdx.x < TS) S[p * TS + threadIdx.x] = s.sgn[threadIdx.x];
+    }
+    const int nr = nb - 1 - p;
+    for (int task = cta; task < 2 * (nb - 1); task += C) {
+      double acc[2][2];
+      if (task < nr) {  // U~(p, j) = L_pp^-1 F(p, j)
+        const int j = p + 1 + task;
+        tile_load_sync(s.a, TRef{tile_ptr(F, bp, p, j), bp, 0});
+        acc_zero(acc);
+        tile_mma(acc, s.di, s.a);
+        acc_to_global(acc, tile_ptr(F, bp, p, j), bp, 1.0);
+      } else if (task < 2 * nr) {  // L(i, p) = F(i, p) U~_pp^-1
+        const int i = p + 1 + (task - nr);
+        tile_load_sync(s.a, TRef{tile_ptr(F, bp, i, p), bp, 0});
+        acc_zero(acc);
+        tile_mma(acc, s.a, s.e);
+        acc_to_global(acc, tile_ptr(F, bp, i, p), bp, 1.0);
+      } else if (task < 2 * nr + p) {  // Ui(k, p) = -(sum_l Ui(k,l) U~(l,p)) U~_pp^-1
+        const int k = task - 2 * nr;
+        tile_sum(acc, p - k, [&](int q, TRef& A, TRef& B) {
+          const int l = k + q;
+          A = TRef{tile_ptr(Ui, bp, k, l), bp, 0};
+          B = TRef{tile_ptr(F, bp, l, p), bp, 0};
+        }, s);
+        acc_to_smem(acc, s.c);
+        acc_zero(acc);
+        tile_mma(acc, s.c, s.e);
+        acc_to_global(acc, tile_ptr(Ui, bp, k, p), bp, -1.0);
+      } else {  // Li(p, k) = -L_pp^-1 (sum_l L(p,l) Li(l,k))
+        const int k = task - 2 * nr - p;
+        tile_sum(acc, p - k, [&](int q, TRef& A, TRef& B) {
+          const int l = k + q;
+          A = TRef{tile_ptr(F, bp, p, l), bp, 0};
+          B = TRef{tile_ptr(Li, bp, l, k), bp, 0};
+        }, s);
+        acc_to_smem(acc, s.c);
+        acc_zero(acc);
+        tile_mma(acc, s.di, s.c);
+        acc_to_global(acc, tile_ptr(Li, bp, p, k), bp, -1.0);
+      }
+      __syncthreads();
+    }
+    cluster_barrier(cl);
+    const int nt = nr * nr;
+    for (int task = cta; task < nt; task += C) {
+      const int i = p + 1 + task % nr, j = p + 1 + task / nr;
+      double acc[2][2];
+      tile_sum(acc, 1, [&](int, TRef& A, TRef& B) {
+        A = TRef{tile_ptr(F, bp, i, p), bp, 0};
+        B = TRef{tile_ptr(F, bp, p, j), bp, 0};
+      }, s);
+      acc_sub_global(acc, tile_ptr(F, bp, i, j), bp);
+      __syncthreads();
+    }
+    cluster_barrier(cl);
+  }
+}
+
+__device__ void init_stats(SmallSm& s) {
+  if (threadIdx.x == 0) {
+    s.bad = 0;
+    s.dmin = DBL_MAX;
+    s.dmax = 0.0;
+  }
+  __syncthreads();
+}
+
+// Identity padding of a Gram written by the GEMM into W (b x b valid, ld bp);
+// zero the strictly-lower tiles of the listed upper-triangular outputs.
+__device__ void init_gram_and_zero(cg::cluster_group& cl, const SmallDims& d, double* W, double* const* zl, int nzl) {
+  const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+  const int bp = d.bp, b = d.b;
+  const int64_t tot = int64_t(bp) * bp;
+  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+    const int r = int(e % bp), c = int(e / bp);
+    if (r >= b || c >= b) W[e] = (r == c) ? 1.0 : 0.0;
+    const int ti = r / TS, tj = c / TS;
+    if (ti > tj)
+      for (int z = 0; z < nzl; ++z) zl[z][e] = 0.0;
+  }
+}
+
+// kernel 1: Cholesky + inverse of the Gram G1 = A^T A.
+// stats[0] = breakdown (0/1), stats[1] = min diag R, stats[2] = max diag R.
+__global__ void __launch_bounds__(SNT, 1)
+chol_inv_k(SmallDims d, double* __restrict__ W, double* __restrict__ R, double* __restrict__ Ri,
+           double* __restrict__ stats) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm_raw[];
+  SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
+  init_stats(s);
+  double* zl[2] = {R, Ri};
+  init_gram_and_zero(cl, d, W, zl, 2);
+  cluster_barrier(cl);
+  chol_inv_dev(cl, d, W, R, Ri, s);
+  if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    stats[0] = s.bad ? 1.0 : 0.0;
+    stats[1] = s.dmin;
+    stats[2] = s.dmax;
+  }
+}
+
+struct ReconArgs {
+  SmallDims d;
+  double* W2;        // Gram of Q1 (b x b valid, ld bp), destroyed
+  const double* R1;  // first-pass factor (bp x bp)
+  const double* Q1;  // Q1 (ld ldq), its top b x b block is read
+  int64_t ldq;
+  double *R2, *R2i, *F, *Li, *Ui, *M, *US, *S;  // bp x bp workspaces (S: bp)
+  const double* stats1;                          // chol_inv_k stats of the first pass
+  double* Rh;                                    // out: R of the panel (b x b, ld ldr)
+  int64_t ldr;
+  double* Tw;                                    // out: compact-WY T (b x b, ld ldt)
+  int64_t ldt;
+  double* tau;                                   // out: b
+  int* flag;                                     // out: 0 = reconstruction valid
+  double dev_max;                                // max |G2 - I| accepted
+};
+
+// kernel 2: second CholeskyQR pass + Householder reconstruction.
+__global__ void __launch_bounds__(SNT, 1) recon_k(ReconArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm_raw[];
+  SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
+  __shared__ double devred[SNT / 32];
+  const SmallDims d = a.d;
+  const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+  const int bp = d.bp, nb = d.nb, b = d.b;
+  init_stats(s);
+  cl.sync();  // every CTA's stats are initialised before any remote update
+  // ---- init: deviation of G2 from I (before padding), padding, zero lower tiles, padded Q block
+  {
+    double dev = 0.0;
+    const int64_t tot = int64_t(bp) * bp;
+    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+      const int r = int(e % bp), c = int(e / bp);
+      if (r < b && c < b) {
+        const double v = a.W2[e] - (r == c ? 1.0 : 0.0);
+        dev = fmax(dev, isfinite(v) ? fabs(v) : 1e300);
+      } else {
+        a.W2[e] = (r == c) ? 1.0 : 0.0;
+      }
+      a.F[e] = (r < b && c < b) ? a.Q1[r + c * a.ldq] : 0.0;  // F <- Q block (negated in the first phase)
+      if (r / TS > c / TS) {
+        a.R2[e] = 0.0;
+        a.R2i[e] = 0.0;
+        a.Ui[e] = 0.0;
+        a.M[e] = 0.0;
+        a.US[e] = 0.0;
+      }
+      if (r / TS < c / TS) a.Li[e] = 0.0;
+    }
+    for (int o = 16; o; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    if ((threadIdx.x & 31) == 0) devred[threadIdx.x >> 5] = dev;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < SNT / 32; ++w) m = fmax(m, devred[w]);
+      if (!(m <= a.dev_max)) atomicOr(cl.map_shared_rank(&s.bad, 0), 1);
+    }
+    __syncthreads();
+  }
+  cluster_barrier(cl);
+  // ---- second Cholesky pass
+  chol_inv_dev(cl, d, a.W2, a.R2, a.R2i, s);
+  // ---- F = -(Q(0:b, :) R2^-1)   (F currently holds the padded Q block; use US as the source copy)
+  {
+    // copy F -> US (source), then F(I,J) = -sum_{K<=J} US(I,K) R2i(K,J)
+    const int64_t tot = int64_t(bp) * bp;
+    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) a.US[e] = a.F[e];
+    cluster_barrier(cl);
+    for (int task = cta; task < nb * nb; task += C) {
+      const int I = task % nb, J = task / nb;
+      double acc[2][2];
+      tile_sum(acc, J + 1, [&](int q, TRef& A, TRef& B) {
+        A = TRef{tile_ptr(a.US, bp, I, q), bp, 0};
+        B = TRef{tile_ptr(a.R2i, bp, q, J), bp, 0};
+      }, s);
+      acc_to_global(acc, tile_ptr(a.F, bp, I, J), bp, -1.0);
+      __syncthreads();
+    }
+    cluster_barrier(cl);
+    // US is reused below: clear its lower tiles again
+    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+      const int r = int(e % bp), c = int(e / bp);
+      if (r / TS > c / TS) a.US[e] = 0.0;
+    }
+  }
+  // ---- sign-modified LU with inverses
+  lu_sign_inv_dev(cl, d, a.F, a.Li, a.Ui, a.S, s);
+  // ---- US = U~ S (upper tiles; lower part of diagonal tiles zeroed)
+  {
+    const int64_t tot = int64_t(bp) * bp;
+    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+      const int r = int(e % bp), c = int(e / bp);
+      if (r / TS <= c / TS) a.US[e] = (r <= c) ? __ldcg(a.F + e) * __ldcg(a.S + c) : 0.0;
+    }
+  }
+  cluster_barrier(cl);
+  // ---- T = US Li^T, M = R2i Ui, Rh = S R2 R1  (upper tile products)
+  {
+    const int nup = nb * (nb + 1) / 2;
+    for (int task = cta; task < 3 * nup; task += C) {
+      const int kind = task / nup;
+      int I, J;
+      upper_pair(task % nup, 0, nb, I, J);
+      double acc[2][2];
+      if (kind == 0) {
+        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
+          const int K = I + q;
+          A = TRef{tile_ptr(a.US, bp, I, K), bp, 0};
+          B = TRef{tile_ptr(a.Li, bp, J, K), bp, 1};
+        }, s);
+        acc_each(acc, [&](int r, int c, double v) {
+          const int gr = I * TS + r, gc = J * TS + c;
+          if (gr < b && gc < b) {
+            a.Tw[gr + gc * a.ldt] = (gr <= gc) ? v : 0.0;
+            if (gr == gc) a.tau[gr] = v;
+          }
+        });
+      } else if (kind == 1) {
+        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
+          const int K = I + q;
+          A = TRef{tile_ptr(a.R2i, bp, I, K), bp, 0};
+          B = TRef{tile_ptr(a.Ui, bp, K, J), bp, 0};
+        }, s);
+        acc_to_global(acc, tile_ptr(a.M, bp, I, J), bp, 1.0);
+      } else {
+        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
+          const int K = I + q;
+          A = TRef{tile_ptr(a.R2, bp, I, K), bp, 0};
+          B = TRef{tile_ptr(a.R1, bp, K, J), bp, 0};
+        }, s);
+        acc_each(acc, [&](int r, int c, double v) {
+          const int gr = I * TS + r, gc = J * TS + c;
+          if (gr < b && gc < b) a.Rh[gr + gc * a.ldr] = (gr <= gc) ? __ldcg(a.S + gr) * v : 0.0;
+        });
+      }
+      __syncthreads();
+    }
+    // strictly-lower tiles of the outputs
+    for (int task = cta; task < nb * nb; task += C) {
+      const int I = task % nb, J = task / nb;
+      if (I <= J) continue;
+      for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+        const int gr = I * TS + (e & 31), gc = J * TS + (e >> 5);
+        if (gr < b && gc < b) {
+          a.Tw[gr + gc * a.ldt] = 0.0;
+          a.Rh[gr + gc * a.ldr] = 0.0;
+        }
+      }
+    }
+  }
+  if (cta == 0 && threadIdx.x == 0) {
+    const bool bad1 = a.stats1[0] != 0.0;
+    *a.flag = (bad1 || s.bad) ? 1 : 0;
+  }
+}
+
+// V(0:b, 0:b) <- unit lower L (strict lower part of F, ld bp)
+__global__ void put_unit_lower_k(int b, const double* __restrict__ F, int bp, double* __restrict__ V, int64_t ldv) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(b) * b;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(e % b), c = int(e / b);
+    V[r + c * ldv] = (r > c) ? F[r + int64_t(c) * bp] : (r == c ? 1.0 : 0.0);
+  }
+}
+
+template <class K, class... Args>
+void launch_cluster(K kern, cudaStream_t st, int C, Args... args) {
+  static bool attr = false;
+  const size_t smem = sizeof(SmallSm);
+  if (!attr) {
+    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(SNT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+}  // namespace
+
+int small_pad(int64_t b) { return (int)cdiv(b, TS) * TS; }
+
+size_t small_work_elems(int64_t b) {
+  const size_t bp = size_t(small_pad(b));
+  return size_t(14) * bp * bp + 2 * bp + 64;
+}
+
+SmallWork carve_small(double* base, int64_t b) {
+  const size_t bp = size_t(small_pad(b)), q = bp * bp;
+  SmallWork w;
+  w.bp = (int)bp;
+  double* p = base;
+  w.W1 = p; p += q;
+  w.R1 = p; p += q;
+  w.R1i = p; p += q;
+  w.W2 = p; p += q;
+  w.R2 = p; p += q;
+  w.R2i = p; p += q;
+  w.F = p; p += q;
+  w.Li = p; p += q;
+  w.Ui = p; p += q;
+  w.M = p; p += q;
+  w.US = p; p += q;
+  w.S = p; p += bp;
+  w.stats = p; p += 16;
+  w.flag = reinterpret_cast<int*>(p); p += 16;
+  return w;
+}
+
+void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w) {
+  SmallDims d{(int)b, w.bp, w.bp / TS};
+  ProfScope _p(st, C_QR_SMALL, 0.0);
+  count_launch(C_QR_SMALL);
+  launch_cluster(chol_inv_k, st, SC, d, w.W1, w.R1, w.R1i, w.stats);
+}
+
+void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt) {
+  ReconArgs a;
+  a.d = SmallDims{(int)b, w.bp, w.bp / TS};
+  a.W2 = w.W2;
+  a.R1 = w.R1;
+  a.Q1 = Q1;
+  a.ldq = ldq;
+  a.R2 = w.R2;
+  a.R2i = w.R2i;
+  a.F = w.F;
+  a.Li = w.Li;
+  a.Ui = w.Ui;
+  a.M = w.M;
+  a.US = w.US;
+  a.S = w.S;
+  a.stats1 = w.stats;
+  a.Rh = R;
+  a.ldr = ldr;
+  a.Tw = Tw;
+  a.ldt = ldt;
+  a.tau = tau;
+  a.flag = w.flag;
+  a.dev_max = 0.5;
+  ProfScope _p(st, C_QR_SMALL, 0.0);
+  count_launch(C_QR_SMALL);
+  launch_cluster(recon_k, st, SC, a);
+}
+
+void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv) {
+  ProfScope _p(st, K_MISC, 0.0);
+  count_launch(K_MISC);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(b * b, 256), 512));
+  put_unit_lower_k<<<blocks, 256, 0, st>>>((int)b, w.F, w.bp, V, ldv);
+  RUTV_LAUNCH_CK();
+}
+
+}  // namespace rutv

@@ -76,11 +76,31 @@ def test_dgemm_misaligned_views():
 
 
 # ----------------------------------------------------------------------------- Householder panel QR
-@pytest.mark.parametrize("m,b", [(40, 8), (500, 50), (1000, 77), (3000, 128), (10000, 256), (20000, 64)])
-def test_panel_qr_vs_oracle(m, b):
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("m,b,decades", [(40, 8, 3), (500, 50, 3), (1000, 77, 3), (3000, 128, 3), (10000, 256, 3),
+                                         (20000, 64, 3), (600, 512, 2), (5000, 200, 12)])
+def test_panel_qr_vs_oracle(m, b, decades, mode):
+    """mode 0 = CholeskyQR2 + Householder reconstruction (R20), mode 1 =
+    column-by-column Householder; both must give the oracle's dlarfg reflectors.
+    A 12-decade panel (kappa ~ 1e12) is beyond CholeskyQR2 and must take the
+    Householder fallback in mode 0."""
     rng = np.random.default_rng(m + b)
-    Y = rng.standard_normal((m, b)) @ np.diag(10.0 ** -np.linspace(0, 3, b))
-    V, R, tau, Tw = P.panel_qr(to_dev(Y))
+    # graded columns mixed by a Haar rotation: kappa(Y) ~ 10^decades even after
+    # column equilibration (column scaling alone leaves CholeskyQR accurate)
+    H, _ = np.linalg.qr(rng.standard_normal((b, b)))
+    Y = rng.standard_normal((m, b)) @ np.diag(10.0 ** -np.linspace(0, decades, b)) @ H
+    V, R, tau, Tw, fb = P.panel_qr(to_dev(Y), mode=mode, return_fallback=True)
+    assert fb == (mode == 0 and decades > 6)
+    if decades > 6:
+        # kappa ~ 1e12: the reflectors themselves are determined only to ~kappa eps;
+        # check the factorization (structure, orthogonality, reconstruction)
+        Vh, Th, Rh = to_host(V), to_host(Tw), to_host(R)
+        assert np.all(np.triu(Vh, 1) == 0) and np.all(np.diag(Vh) == 1) and np.all(np.tril(Rh, -1) == 0)
+        Q1 = np.eye(m, b) - Vh @ (Th @ Vh[:b].T)
+        assert np.linalg.norm(Q1.T @ Q1 - np.eye(b)) < 1e-13 * math.sqrt(m) * 10
+        assert np.linalg.norm(Q1 @ Rh - Y) <= 1e-13 * np.linalg.norm(Y) * 10
+        assert np.all((to_host(tau) >= 1.0) & (to_host(tau) <= 2.0))
+        return
     F, tau_o = oracle.geqr2(Y)
     Vo = oracle.unit_lower(F, b)
     To = oracle.larft(Vo, tau_o)
@@ -155,13 +175,15 @@ PARITY = [
 ]
 
 
-@pytest.mark.parametrize("name,scale,q,uv", PARITY)
-def test_randutv_parity(name, scale, q, uv):
+@pytest.mark.parametrize("name,scale,q,uv,qr_mode", [p + (0,) for p in PARITY] + [
+    ("c2", 0.2, 2, True, 1), ("c3", 0.1, None, False, 1), ("c4", 0.05, None, True, 1)])
+def test_randutv_parity(name, scale, q, uv, qr_mode):
+    """qr_mode 0: CholeskyQR2 + reconstruction panel QRs (default); 1: Householder."""
     c = testmat.config(name, scale=scale, q=q)
     A = c.A
     m, n = A.shape
     ref = oracle.randutv(A, c.b, c.q, c.seed, build_ortho=uv)
-    U, T, V, info = P.randutv(to_dev(A), c.b, c.q, c.seed, with_uv=uv)
+    U, T, V, info = P.randutv(to_dev(A), c.b, c.q, c.seed, with_uv=uv, qr_mode=qr_mode)
     torch.cuda.synchronize()
     Th = to_host(T)
     par = check_parity(Th, ref["T"], ref["a_fro"])
