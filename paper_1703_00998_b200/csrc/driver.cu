@@ -153,6 +153,22 @@ void dg(const Work& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, 
   dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems);
 }
 
+// Low-priority side stream per device for work off the critical path (the
+// deferred b x b SVDs): its kernels fill the SMs the latency-bound panel-QR
+// kernels leave idle, and the block scheduler prefers the main stream's CTAs.
+cudaStream_t side_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, least));
+  }
+  return streams[dev];
+}
+
 int check_qr(int rc) {
   if (rc != OK) throw rc;
   return rc;
@@ -187,6 +203,26 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
 
   int64_t steps = 0, k_done = 0;
   bool final_block = false, final_tall = false;
+  // The b x b SVDs of R11 are independent of later steps (R13): with
+  // the single-cluster Jacobi kernel they run in chunks on the side stream.
+  constexpr int64_t kSvdChunk = 8;
+  const bool svd_side = jacobi_single_launch((int)b);
+  cudaStream_t side = svd_side ? side_stream() : nullptr;
+  int64_t svd_done = 0;
+  std::vector<cudaEvent_t> evs;
+  auto launch_svd_chunk = [&]() {
+    if (steps <= svd_done) return;
+    cudaEvent_t e;
+    RUTV_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+    RUTV_CK(cudaEventRecord(e, st));
+    RUTV_CK(cudaStreamWaitEvent(side, e, 0));
+    const int64_t s0 = svd_done, cnt = steps - svd_done;
+    jacobi_svd_batched(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, w.Dall + s0 * b,
+                       w.Usall + size_t(s0) * b * b, w.Vsall + size_t(s0) * b * b,
+                       w.jwork + jacobi_work_elems((int)s0, (int)b), w.sweeps + s0);
+    svd_done = steps;
+  };
   int64_t r0f = 0, nif = 0, mif = 0;
   double trailing = 0.0;
   bool stopped = false;
@@ -252,6 +288,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       dg(w, st, false, true, mi, nc, b, -1.0, Wu, ldwu, w.Wt2, n, 1.0, Cm, m);      // C -= W_u (.)^T
       ++steps;
       k_done = f2;
+      if (svd_side && steps - svd_done >= kSvdChunk) launch_svd_chunk();
       if (o.tol > 0.0) {
         double t2 = 0.0;
         fro2(st, m - e2, n - f2, T + e2 + f2 * m, m, w.nrm, w.scal);
@@ -282,8 +319,19 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   set_gemm_role(C_GEMM_OTHER);
   // ---- batched small SVDs
   int max_sweeps = 0;
-  if (steps > 0)
+  if (svd_side) {
+    launch_svd_chunk();
+    if (!evs.empty()) {
+      cudaEvent_t e;
+      RUTV_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      RUTV_CK(cudaEventRecord(e, side));
+      RUTV_CK(cudaStreamWaitEvent(st, e, 0));
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  } else if (steps > 0) {
     jacobi_svd_batched(st, (int)steps, (int)b, w.Rall, b, b * b, w.Dall, w.Usall, w.Vsall, w.jwork, w.sweeps);
+  }
   if (final_block)
     jacobi_svd_batched(st, 1, (int)nif, w.Rfin, nif, nif * nif, w.Dfin, w.Usfin, w.Vsfin, w.jworkf,
                        w.sweeps + steps);

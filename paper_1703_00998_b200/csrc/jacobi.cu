@@ -361,6 +361,11 @@ JacobiDesc make_desc(int k) {
 }
 }  // namespace
 
+bool jacobi_single_launch(int k) {
+  JacobiDesc d = make_desc(k);
+  return k > 1 && d.nb / 2 <= 8;
+}
+
 size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 1); }
 
 void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,

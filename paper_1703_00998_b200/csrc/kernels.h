@@ -125,6 +125,8 @@ int qr_max_rows();
 // R + i*strideR, ld ldr):  R_i = Us_i diag(D_i) Vs_i^T, D_i non-increasing.
 // Works on B = R_i^T.  work needs 2*batch*k*k doubles.
 size_t jacobi_work_elems(int batch, int k);
+// true when a k x k SVD runs as one cluster launch without host synchronisation
+bool jacobi_single_launch(int k);
 void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
                         double* D, double* Us, double* Vs, double* work, int* sweeps_out);
 
