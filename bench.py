@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-utv", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the distributed (NCCL, block-cyclic) path even at N=1")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = c3 recipe at n = 10000 N^(1/3) (fixed flops per GPU); strong = fixed c3")
     return ap.parse_args()
 
 
@@ -146,9 +150,9 @@ def oracle_sample(A_host, case, reps=1):
     return f / t / 1e9, t, f, cores
 
 
-def make_input(case_name, device, rank):
+def make_input(case_name, device, rank, scale=1.0):
     import testmat
-    At, case = testmat.device_config(case_name, device=device)
+    At, case = testmat.device_config(case_name, device=device, scale=scale)
     return At, case
 
 
@@ -197,28 +201,42 @@ def main():
     import numpy as np
     import torch
     import paper_1703_00998_b200 as P
+    from paper_1703_00998_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    use_dist = world > 1 or args.dist
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    if use_dist:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    scaling = args.scaling if world > 1 else "weak"
+    scale = world ** (1.0 / 3.0) if (world > 1 and scaling == "weak") else 1.0
 
-    At, case = make_input(args.config, dev, rank)
+    At, case = make_input(args.config, dev, rank, scale)
     A = At.t()
     m, n = A.shape
     F = flops_for(case, m, n)
-    T = P.empty_cm(m, n, dev)
     stream = torch.cuda.current_stream(dev)
+    if use_dist:
+        comm = D.nccl_from_torch()
+        S = D.shard(A, case.b, rank, world)
+        A_host_src = S
+        del A, At
+        torch.cuda.empty_cache()
+        Tsh = [P.empty_cm(m, S.shape[1], dev)]
 
-    def step(with_uv=False, out=None):
-        return P.randutv(A, case.b, case.q, case.seed, k_stop=case.k_stop, tol=case.tol, with_uv=with_uv,
-                         out=out if out is not None else (None, T, None))
+        def step(with_uv=False, out=None):
+            return D.factor(comm, [S], m, n, case.b, case.q, case.seed, k_stop=case.k_stop, tol=case.tol, out=Tsh)
+    else:
+        T = P.empty_cm(m, n, dev)
+
+        def step(with_uv=False, out=None):
+            return P.randutv(A, case.b, case.q, case.seed, k_stop=case.k_stop, tol=case.tol, with_uv=with_uv,
+                             out=out if out is not None else (None, T, None))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -244,10 +262,12 @@ def main():
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms, float(launches)], device=dev, dtype=torch.float64)
+        tl = t.clone()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * F / (ms * 1e-3) / 1e9
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        ms, launches = float(t[0].item()), int(tl[1].item())
+    value = F / (ms * 1e-3) / 1e9  # whole-job flops (the factorization's flop count) / time
 
     # ---------------------------------------------------------------- roofline of the dominant kernel class
     P.profile_begin()
@@ -277,10 +297,12 @@ def main():
                          if v["ms"] > 0 and v["flops"] > 0 else None, "launches": v["launches"]}
                      for k, v in prof.items()},
     }
+    if use_dist:
+        roofline["note"] = "rank 0's kernels; per-class event times include waits on collectives"
 
-    # ---------------------------------------------------------------- U,V formed (context)
+    # ---------------------------------------------------------------- U,V formed (context, single GPU)
     utv = None
-    if not args.no_utv and rank == 0:
+    if not args.no_utv and not use_dist:
         U = P.empty_cm(m, m, dev)
         V = P.empty_cm(n, n, dev)
         step(True, (U, T, V))
@@ -296,35 +318,56 @@ def main():
         del U, V
         torch.cuda.empty_cache()
 
-    # ---------------------------------------------------------------- end to end through the C ABI, host buffers
+    # ---------------------------------------------------------------- end to end, host buffers in the timed region
     e2e = None
     if not args.no_e2e:
-        Ah = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
-        Ah.copy_(At)
-        Th = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
-        torch.cuda.synchronize(dev)
-        P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None, Th.data_ptr(), None)
-        if dist:
-            dist.barrier()
         reps = max(1, min(args.steps, 3))
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            rc = P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None, Th.data_ptr(),
-                              None)
-            assert rc == 0, rc
-        te = (time.perf_counter() - t0) / reps
-        if dist:
+        if use_dist:
+            # per rank: pinned host shard -> device, distributed factorization, T shard -> host
+            nl = A_host_src.shape[1]
+            Ah = torch.empty(nl, m, dtype=torch.float64, pin_memory=True)
+            Ah.copy_(A_host_src.t())
+            Th = torch.empty(nl, m, dtype=torch.float64, pin_memory=True)
+            Sd = P.empty_cm(m, nl, dev)
+
+            def e2e_step():
+                Sd.t().copy_(Ah, non_blocking=True)
+                D.factor(comm, [Sd], m, n, case.b, case.q, case.seed, k_stop=case.k_stop, tol=case.tol, out=Tsh)
+                Th.copy_(Tsh[0].t(), non_blocking=True)
+                torch.cuda.synchronize(dev)
+            e2e_step()
+            dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                e2e_step()
+            te = (time.perf_counter() - t0) / reps
             t = torch.tensor([te], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": round(world * F / te / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": m * n * 8,
-               "d2h_bytes_per_step": m * n * 8, "ms_per_step": round(te * 1e3, 3),
-               "timer": "host wall clock around the synchronous randutv_factor call (pinned host A and T)"}
-        del Ah, Th
+            hb = tb = m * nl * 8
+            del Ah, Th, Sd
+        else:
+            Ah = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+            Ah.copy_(At)
+            Th = torch.empty(n, m, dtype=torch.float64, pin_memory=True)
+            torch.cuda.synchronize(dev)
+            P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None, Th.data_ptr(), None)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                rc = P.factor_raw(m, n, Ah.data_ptr(), m, case.b, case.q, case.seed, case.k_stop, None,
+                                  Th.data_ptr(), None)
+                assert rc == 0, rc
+            te = (time.perf_counter() - t0) / reps
+            hb = tb = m * n * 8
+            del Ah, Th
+        e2e = {"value": round(F / te / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": hb,
+               "d2h_bytes_per_step": tb, "ms_per_step": round(te * 1e3, 3),
+               "timer": "host wall clock (max over ranks) around H2D of A, the factorization and D2H of T"
+                        + (" (per-rank shards, bytes per rank)" if use_dist else " (randutv_factor on pinned host A, T)")}
 
     # ---------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and rank == 0:
+    if not args.no_cpu_baseline and world == 1 and rank == 0 and not use_dist:
         A_host = np.asfortranarray(A.cpu().numpy())
         v, t, f, cores = oracle_sample(A_host, case)
         cpu = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -332,11 +375,16 @@ def main():
                          f"on the same {m}x{n} input: {f:.3e} flops in {t:.2f} s"}
 
     if rank == 0:
+        if use_dist:
+            par = f"block-cyclic columns (b={case.b}) x{world}, NCCL"
+        else:
+            par = "single"
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": scaling if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(workload_desc(case, m, n), parallelism=f"replicas x{world}" if world > 1 else "single"),
+            "config": dict(workload_desc(case, m, n), parallelism=par),
             "pct_fp64_peak": round(100 * value / world / 1e3 / FP64_DMMA_PEAK_TFLOPS, 2),
             "pct_cublas_dgemm": round(100 * value / world / 1e3 / FP64_CUBLAS_DGEMM_TFLOPS, 2),
             "time_to_factor_s": round(ms * 1e-3, 4),
@@ -346,6 +394,7 @@ def main():
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
 
 

@@ -156,6 +156,56 @@ RANDUTV_API int randutv_small_svd_batched(int32_t batch, int32_t k, const double
                               double* Us, double* Vs, int32_t* sweeps, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Multi-GPU.  A and T are distributed in 1-D
+ * block-cyclic column blocks of width b: global column block j (columns
+ * j*b .. min((j+1)b, n)-1) lives on rank j mod nranks; a rank stores its blocks
+ * in increasing j, contiguously, as an m x n_loc column-major matrix
+ * (n_loc = randutv_dist_local_cols).  Per step the ranks exchange, through the
+ * communicator: the b x b Grams of the CholeskyQR steps, Z = X Y (m_i x b),
+ * the top b x b block of Q1, P = T(:,J) W_v (m x b) (allreduce), and the
+ * panel's (W_u, T_u, R11) (broadcast from the owner of the block).
+ * ------------------------------------------------------------------------ */
+#define RANDUTV_NCCL_ID_BYTES 128
+typedef struct randutv_comm randutv_comm;
+
+/* 128-byte NCCL unique id (rank 0 creates it; the caller distributes it, e.g.
+ * with torch.distributed).  NCCL is loaded at run time (the process's
+ * libnccl.so.2, e.g. torch's); RANDUTV_ERR_NCCL if unavailable. */
+RANDUTV_API int randutv_nccl_unique_id(void* id_out);
+/* NCCL communicator for ``rank`` of ``nranks`` on the current CUDA device
+ * (collective: every rank must call it).  Released by randutv_comm_destroy. */
+RANDUTV_API int randutv_comm_init_nccl(int32_t nranks, int32_t rank, const void* id, randutv_comm** out);
+/* Loopback communicator: this process drives all ``nranks`` ranks on the
+ * current device, each with its own shard; collectives are device copies/sums
+ * in fixed rank order between bulk-synchronous phases (no kernel waits on
+ * another rank).  It checks the distributed arithmetic on one GPU. */
+RANDUTV_API int randutv_comm_init_loopback(int32_t nranks, randutv_comm** out);
+RANDUTV_API int randutv_comm_destroy(randutv_comm* comm);
+/* Ranks driven by this process: returns their count (1 for NCCL, nranks for
+ * loopback), writes the world size and up to max_ranks rank ids. */
+RANDUTV_API int randutv_comm_local_ranks(const randutv_comm* comm, int32_t* world, int32_t* ranks_out,
+                                         int32_t max_ranks);
+/* Host-only layout queries (no GPU): local column count of ``rank`` and the
+ * global column of a rank's local column; -1 on invalid arguments. */
+RANDUTV_API int64_t randutv_dist_local_cols(int64_t n, int64_t b, int32_t rank, int32_t nranks);
+RANDUTV_API int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_t rank, int32_t nranks);
+
+/* Distributed randutv_factor_ex, T-only mode (U = V = NULL; the paper's "no
+ * orthonormal matrices" mode).  A_loc[l], T_loc[l] (device,
+ * ld lda_loc[l] / ldt_loc[l] >= m) are the shards of the l-th rank this
+ * process drives (randutv_comm_local_ranks order).  T_loc may alias A_loc.
+ * All ranks must pass identical m, n, b, q, seed, k_stop and options.  On
+ * return each T_loc holds that rank's columns of T; info is identical on all
+ * ranks.  Errors: -1 opts, -2 comm, -3 m, -4 n, -5 A_loc/lda_loc, -7 b, -8 q,
+ * -10 k_stop, -11 T_loc/ldt_loc; RANDUTV_ERR_NCCL on a failed collective.
+ * Synchronises the stream as randutv_factor_ex does, plus once per step for
+ * the (rank-consistent) CholeskyQR fallback decisions. */
+RANDUTV_API int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m, int64_t n,
+                                    const double* const* A_loc, const int64_t* lda_loc, int64_t b, int32_t q,
+                                    uint64_t seed, int64_t k_stop, double* const* T_loc, const int64_t* ldt_loc,
+                                    randutv_info* info);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation (used by bench.py).
  * ------------------------------------------------------------------------ */
 

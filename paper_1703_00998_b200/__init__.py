@@ -97,7 +97,10 @@ def lib():
 EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
             "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
             "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
-            "randutv_profile_end", "randutv_profile_class_name"]
+            "randutv_profile_end", "randutv_profile_class_name", "randutv_nccl_unique_id",
+            "randutv_comm_init_nccl", "randutv_comm_init_loopback", "randutv_comm_destroy",
+            "randutv_comm_local_ranks", "randutv_dist_local_cols", "randutv_dist_global_col",
+            "randutv_factor_dist"]
 
 
 def launch_count() -> int:

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_randutv.so")
-SOURCES = ["gemm.cu", "misc.cu", "qr.cu", "smallmat.cu", "jacobi.cu", "prof.cu", "driver.cu"]
+SOURCES = ["gemm.cu", "misc.cu", "qr.cu", "smallmat.cu", "dist.cu", "jacobi.cu", "prof.cu", "driver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr"]
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
-    subprocess.check_call([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
+    subprocess.check_call([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,0 +1,853 @@
+// Multi-GPU randUTV: A, T in 1-D block-cyclic
+// column blocks of width b (block j on rank j mod P), T-only mode.
+//
+// Every step of Fig. fig:randUTV maps onto rank-local DMMA
+// GEMMs plus a fixed set of collectives per step:
+//   sketch      G_i on every rank (Philox, no communication);  Y_loc = X_loc^T G
+//   power loop  C1  allreduce of the b x b Gram (CholeskyQR re-orthonormalization)
+//               C1' allreduce of Z = X Y = sum_r X_loc Y_loc  (m_i x b)
+//   QR(Y)       C2  allreduce of the two Grams + broadcast of the top b x b block
+//               of Q1 from the owner of block i; the reconstruction runs
+//               redundantly (deterministically) on every rank, so W_v stays
+//               distributed by rows exactly like the columns of X
+//   right apply C3  allreduce of P = T(:,J) W_v = sum_r T_loc W_v,loc  (m x b)
+//   panel QR    C4  broadcast of (W_u, T_u, R11) from the owner of block i
+//   left apply  local;   early stop: allreduce of the trailing ||.||_F^2
+// The b x b SVDs (R11 is on every rank) and their folds run after the loop:
+// the row folds T(I2,J3) <- Us^T T(I2,J3) on every rank's local columns, the
+// column folds T(I1,J2) <- T(I1,J2) Vs on the owner.
+//
+// Collectives go through a small interface with two implementations: NCCL (one
+// process per GPU; the symbols are resolved with dlopen from the libnccl the
+// process already loaded, e.g. torch's) and a loopback that drives P virtual
+// ranks on ONE device with host-ordered collectives (bulk-synchronous phases:
+// no kernel ever waits on another rank) -- the latter exists to check the
+// distributed arithmetic against the oracle on a single GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "../../include/randutv.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace rutv;
+
+// ----------------------------------------------------------------------------- block-cyclic layout
+namespace {
+inline int64_t nblocks(int64_t n, int64_t b) { return cdiv(n, b); }
+// local column count of rank r
+inline int64_t local_cols(int64_t n, int64_t b, int r, int P) {
+  const int64_t nb = nblocks(n, b);
+  int64_t c = 0;
+  for (int64_t j = r; j < nb; j += P) c += std::min(b, n - j * b);
+  return c;
+}
+// number of blocks of rank r with global index < p
+inline int64_t blocks_before(int64_t p, int r, int P) { return (p > r) ? (p - r + P - 1) / P : 0; }
+}  // namespace
+
+// ----------------------------------------------------------------------------- communicators
+namespace rutv {
+
+struct Comm {
+  virtual ~Comm() {}
+  int P = 1;                // world size
+  std::vector<int> ranks;   // global ranks this process drives (1 for NCCL, P for loopback)
+  int dev = 0;
+  // in-place sum over all ranks of bufs[l] (count doubles each)
+  virtual void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) = 0;
+  // bufs[l] <- bufs[root]
+  virtual void bcast(const std::vector<double*>& bufs, size_t count, int root, cudaStream_t st) = 0;
+  // recv[l] = concat over ranks of send[.] (count each)
+  virtual void allgather(const std::vector<double*>& send, const std::vector<double*>& recv, size_t count,
+                         cudaStream_t st) = 0;
+};
+
+namespace {
+__global__ void add_k(size_t n, const double* __restrict__ s, double* __restrict__ d) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    d[i] += s[i];
+}
+void add_into(cudaStream_t st, size_t n, const double* s, double* d) {
+  if (n == 0) return;
+  const int blocks = (int)std::min<size_t>((n + 255) / 256, 2048);
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); add_k<<<blocks, 256, 0, st>>>(n, s, d); }
+  RUTV_LAUNCH_CK();
+}
+
+struct LoopComm : Comm {
+  explicit LoopComm(int p) {
+    P = p;
+    for (int r = 0; r < p; ++r) ranks.push_back(r);
+    RUTV_CK(cudaGetDevice(&dev));
+  }
+  void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) override {
+    // fixed order: ((b0 + b1) + b2) + ...  accumulated in b0, then copied out
+    for (int r = 1; r < P; ++r) add_into(st, count, bufs[r], bufs[0]);
+    for (int r = 1; r < P; ++r)
+      if (count) RUTV_CK(cudaMemcpyAsync(bufs[r], bufs[0], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  void bcast(const std::vector<double*>& bufs, size_t count, int root, cudaStream_t st) override {
+    for (int r = 0; r < P; ++r)
+      if (r != root && count)
+        RUTV_CK(cudaMemcpyAsync(bufs[r], bufs[root], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  void allgather(const std::vector<double*>& send, const std::vector<double*>& recv, size_t count,
+                 cudaStream_t st) override {
+    for (int l = 0; l < P; ++l)
+      for (int r = 0; r < P; ++r)
+        if (count)
+          RUTV_CK(cudaMemcpyAsync(recv[l] + size_t(r) * count, send[r], count * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, st));
+  }
+};
+
+// NCCL entry points, resolved at run time (no link-time dependency on libnccl)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
+             api.AllGather;
+  });
+  return api;
+}
+
+struct NcclError {
+  ncclResult_t r;
+};
+#define RUTV_NCCL(x)                            \
+  do {                                          \
+    ncclResult_t _r = (x);                      \
+    if (_r != ncclSuccess) throw NcclError{_r}; \
+  } while (0)
+
+struct NcclComm : Comm {
+  ncclComm_t c = nullptr;
+  NcclComm(int p, int rank, const ncclUniqueId& id) {
+    P = p;
+    ranks.push_back(rank);
+    RUTV_CK(cudaGetDevice(&dev));
+    RUTV_NCCL(nccl().CommInitRank(&c, p, id, rank));
+  }
+  ~NcclComm() override {
+    if (c) nccl().CommDestroy(c);
+  }
+  void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) override {
+    if (count) RUTV_NCCL(nccl().AllReduce(bufs[0], bufs[0], count, ncclFloat64, ncclSum, c, st));
+  }
+  void bcast(const std::vector<double*>& bufs, size_t count, int root, cudaStream_t st) override {
+    if (count) RUTV_NCCL(nccl().Broadcast(bufs[0], bufs[0], count, ncclFloat64, root, c, st));
+  }
+  void allgather(const std::vector<double*>& send, const std::vector<double*>& recv, size_t count,
+                 cudaStream_t st) override {
+    if (count) RUTV_NCCL(nccl().AllGather(send[0], recv[0], count, ncclFloat64, c, st));
+  }
+};
+
+// ----------------------------------------------------------------------------- helper kernels
+// full (global trailing order) <-> per-rank pieces of the block-cyclic rows of Y:
+// global trailing row t*b + i (block j = p + t, owner r = j mod P, local block
+// k = (j - first_r)/P) <-> piece r, local row k*b + i.
+__global__ void gather_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p, int P, const double* __restrict__ pieces,
+                              int64_t piece_rows, double* __restrict__ full, int64_t ldf) {
+  const int64_t tot = nrows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gr = e % nrows, c = e / nrows;
+    const int64_t t = gr / b, i = gr % b, j = p + t;
+    const int r = int(j % P);
+    const int64_t first = p + ((r - p) % P + P) % P;
+    const int64_t k = (j - first) / P;
+    full[gr + c * ldf] = pieces[int64_t(r) * piece_rows * cols + (k * b + i) + c * piece_rows];
+  }
+}
+__global__ void scatter_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p, int P, int r,
+                               const double* __restrict__ full, int64_t ldf, double* __restrict__ loc, int64_t ldl) {
+  // local rows of rank r: its blocks j >= p in order
+  const int64_t first = p + ((r - p) % P + P) % P;
+  const int64_t tot = nrows * cols;  // nrows = global trailing rows; only rank-r rows are written
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gr = e % nrows, c = e / nrows;
+    const int64_t t = gr / b, i = gr % b, j = p + t;
+    if (j % P != r) continue;
+    const int64_t k = (j - first) / P;
+    loc[(k * b + i) + c * ldl] = full[gr + c * ldf];
+  }
+}
+inline int grid_for_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2048)); }
+}  // namespace
+
+// ----------------------------------------------------------------------------- the distributed driver
+namespace {
+
+struct RankWork {
+  // shapes: m rows; nl = local columns
+  double *G, *Y, *Y2, *Z, *P, *P2, *S, *S2, *pack, *q1, *small, *part, *fold;
+  double *Rall, *Dall, *Usall, *Vsall, *jwork;
+  double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf, *Tfin, *tau, *Ttmp, *Rtmp;
+  double *piece, *gath, *Yfull, *scal, *nrm;
+  int* flag;
+  int* sweeps;
+  size_t part_elems;
+  QrWork qw;
+};
+
+struct DistPlan {
+  int64_t m, n, b, s, nrand, nl_max, maxpiece;
+  int P;
+};
+
+RankWork carve_rank(Arena& ar, const DistPlan& d) {
+  RankWork w{};
+  const int64_t m = d.m, b = d.b, nl = std::max<int64_t>(d.nl_max, 1), mx = std::max(m, d.n);
+  const int64_t sb = std::max<int64_t>(d.nrand, 1);
+  w.G = ar.take<double>(size_t(m) * b);
+  w.Y = ar.take<double>(size_t(nl) * b);
+  w.Y2 = ar.take<double>(size_t(nl) * b);
+  w.Z = ar.take<double>(size_t(m) * b);
+  w.P = ar.take<double>(size_t(m) * b);
+  w.P2 = ar.take<double>(size_t(m) * b);
+  w.S = ar.take<double>(size_t(nl) * b);
+  w.S2 = ar.take<double>(size_t(nl) * b);
+  w.pack = ar.take<double>(size_t(m) * b + 2 * size_t(b) * b + 64);
+  w.q1 = ar.take<double>(size_t(mx) * b);
+  w.small = ar.take<double>(small_work_elems(b));
+  w.part_elems = size_t(8) * mx * b + size_t(148) * 32 * 1024;
+  w.part = ar.take<double>(w.part_elems);
+  w.fold = ar.take<double>(size_t(mx) * b);
+  w.Rall = ar.take<double>(size_t(sb) * b * b);
+  w.Dall = ar.take<double>(size_t(sb) * b);
+  w.Usall = ar.take<double>(size_t(sb) * b * b);
+  w.Vsall = ar.take<double>(size_t(sb) * b * b);
+  w.jwork = ar.take<double>(jacobi_work_elems((int)sb, (int)b));
+  w.Rfin = ar.take<double>(size_t(b) * b);
+  w.Dfin = ar.take<double>(size_t(b));
+  w.Usfin = ar.take<double>(size_t(b) * b);
+  w.Vsfin = ar.take<double>(size_t(b) * b);
+  w.jworkf = ar.take<double>(jacobi_work_elems(1, (int)b));
+  w.Tfin = ar.take<double>(size_t(b) * b);
+  w.tau = ar.take<double>(size_t(b));
+  w.Ttmp = ar.take<double>(size_t(b) * b);
+  w.Rtmp = ar.take<double>(size_t(b) * b);
+  w.piece = ar.take<double>(size_t(d.maxpiece) * b + 1);
+  w.gath = ar.take<double>(size_t(d.P) * d.maxpiece * b + 1);
+  w.Yfull = ar.take<double>(size_t(d.n) * b);
+  w.scal = ar.take<double>(16);
+  w.nrm = ar.take<double>(8192);
+  w.flag = ar.take<int>(16);
+  w.sweeps = ar.take<int>(size_t(sb) + 16);
+  w.qw.part = w.part;
+  w.qw.part_elems = w.part_elems;
+  w.qw.sfull = ar.take<double>(size_t(32) * b);
+  w.qw.s2 = ar.take<double>(size_t(32) * b);
+  w.qw.z = ar.take<double>(size_t(32) * b);
+  w.qw.q1 = w.q1;
+  w.qw.q1_elems = size_t(mx) * b;
+  w.qw.small = w.small;
+  return w;
+}
+
+DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P) {
+  DistPlan d;
+  d.m = m;
+  d.n = n;
+  d.b = b;
+  d.P = P;
+  d.s = std::min(cdiv(m, b), cdiv(n, b));
+  d.nrand = 0;
+  for (int64_t i = 1; i <= d.s; ++i)
+    if (b * i < m && b * i < n) d.nrand = i;
+  d.nl_max = 0;
+  for (int r = 0; r < P; ++r) d.nl_max = std::max(d.nl_max, local_cols(n, b, r, P));
+  d.maxpiece = std::max<int64_t>(d.nl_max, 1);
+  return d;
+}
+
+size_t dist_rank_bytes(const DistPlan& d) {
+  Arena ar;
+  ar.dry = true;
+  carve_rank(ar, d);
+  return ar.off + 4096;
+}
+
+struct LocalRank {
+  int r;                 // global rank
+  const double* A;
+  int64_t lda;
+  double* T;
+  int64_t ldt;
+  int64_t nl;            // local columns
+  RankWork w;
+  SmallWork sw;
+};
+
+void dg(const RankWork& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+        const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems);
+}
+
+int read_int_sync(cudaStream_t st, const int* d) {
+  int h = 0;
+  RUTV_CK(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RUTV_CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+class DistFactor {
+ public:
+  DistFactor(Comm& c, const randutv_opts& o, int64_t m, int64_t n, int64_t b, int q, uint64_t seed,
+             int64_t k_stop, std::vector<LocalRank>& L)
+      : comm(c), o(o), m(m), n(n), b(b), q(q), seed(seed), k_stop(k_stop), L(L), P(c.P) {
+    st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+  }
+
+  int run(randutv_info* info);
+
+ private:
+  Comm& comm;
+  const randutv_opts& o;
+  int64_t m, n, b;
+  int q;
+  uint64_t seed;
+  int64_t k_stop;
+  std::vector<LocalRank>& L;
+  int P;
+  cudaStream_t st;
+  int fallbacks = 0;
+  double a_fro_ = 0.0;
+  std::vector<double*> bufs(double* RankWork::*member) {
+    std::vector<double*> v;
+    for (auto& lr : L) v.push_back(lr.w.*member);
+    return v;
+  }
+
+  // Gram of the distributed n_i x b matrix held in `src` (local rows nt) -> W1 of
+  // every rank's small workspace (allreduced), then chol_inv (redundant).
+  void dist_gram_chol(double* RankWork::*src, const std::vector<int64_t>& nt, int which /*1: W1, 2: W2*/) {
+    const int bp = small_pad(b);
+    for (size_t l = 0; l < L.size(); ++l) {  // packed b x b (ld b) Gram, allreduced, then into the padded slot
+      auto& lr = L[l];
+      dg(lr.w, st, true, false, b, b, nt[l], 1.0, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.*src,
+         std::max<int64_t>(nt[l], 1), 0.0, lr.w.pack, b);
+    }
+    comm.allreduce(bufs(&RankWork::pack), size_t(b) * b, st);
+    for (auto& lr : L) {
+      double* dst = (which == 1) ? lr.sw.W1 : lr.sw.W2;
+      copy_matrix(st, b, b, lr.w.pack, b, dst, bp);
+    }
+    if (which == 1)
+      for (auto& lr : L) small_chol_inv(st, b, lr.sw);
+  }
+
+  // Householder fallback for a distributed Y: allgather -> full Y on every rank,
+  // panel QR there (redundant), then every rank takes its rows of the result.
+  // mode 0: thin Q -> dst (re-orthonormalisation); mode 1: reflectors -> dst, Tv.
+  int dist_householder(int64_t p, int64_t ni, double* RankWork::*src, double* RankWork::*dst,
+                       const std::vector<int64_t>& nt, int mode, double* const* Tv) {
+    int64_t maxpiece = 0;
+    for (int r = 0; r < P; ++r) maxpiece = std::max(maxpiece, local_cols(n, b, r, P) - b * blocks_before(p, r, P));
+    maxpiece = std::max<int64_t>(maxpiece, 1);
+    for (size_t l = 0; l < L.size(); ++l) {
+      auto& lr = L[l];
+      set_zero(st, maxpiece, b, lr.w.piece, maxpiece);
+      copy_matrix(st, nt[l], b, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.piece, maxpiece);
+    }
+    comm.allgather(bufs(&RankWork::piece), bufs(&RankWork::gath), size_t(maxpiece) * b, st);
+    for (size_t l = 0; l < L.size(); ++l) {
+      auto& lr = L[l];
+      {
+        ProfScope _p(st, K_MISC, 0.0);
+        count_launch(K_MISC);
+        gather_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.w.gath, maxpiece, lr.w.Yfull, ni);
+        RUTV_LAUNCH_CK();
+      }
+      QrWork qw = lr.w.qw;
+      qw.mode = 1;
+      int rc = panel_qr(st, ni, b, lr.w.Yfull, ni, lr.w.Rtmp, b, lr.w.tau, mode == 1 ? Tv[l] : lr.w.Ttmp, b, qw);
+      if (rc != OK) return rc;
+      double* out = lr.w.Yfull;
+      if (mode == 0) {  // thin Q into q1 (ni x b), then scatter
+        thin_q(st, ni, b, lr.w.Yfull, ni, lr.w.Ttmp, b, lr.w.q1, ni, lr.w.Rtmp, lr.w.part, lr.w.part_elems);
+        out = lr.w.q1;
+      }
+      {
+        ProfScope _p(st, K_MISC, 0.0);
+        count_launch(K_MISC);
+        scatter_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.r, out, ni, lr.w.*dst,
+                                                            std::max<int64_t>(nt[l], 1));
+        RUTV_LAUNCH_CK();
+      }
+    }
+    ++fallbacks;
+    return OK;
+  }
+};
+
+int DistFactor::run(randutv_info* info) {
+  const bool reortho = (o.no_reortho == 0);
+  const int64_t s = std::min(cdiv(m, b), cdiv(n, b));
+  const int bp = small_pad(b);
+
+  // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
+  for (auto& lr : L) {
+    RUTV_CK(cudaMemsetAsync(lr.w.flag, 0, sizeof(int), st));
+    if (lr.nl > 0) {
+      copy_norm_check(st, m, lr.nl, lr.A, lr.lda, lr.T, lr.ldt, lr.w.nrm, lr.w.scal, lr.w.flag);
+    } else {
+      RUTV_CK(cudaMemsetAsync(lr.w.scal, 0, sizeof(double), st));
+    }
+  }
+  {
+    // pack [sum of squares, non-finite flag] and allreduce
+    for (auto& lr : L) {
+      RUTV_CK(cudaMemcpyAsync(lr.w.pack, lr.w.scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
+      int hf = read_int_sync(st, lr.w.flag);
+      double fv = hf ? 1.0 : 0.0;
+      RUTV_CK(cudaMemcpyAsync(lr.w.pack + 1, &fv, sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    comm.allreduce(bufs(&RankWork::pack), 2, st);
+    double h[2];
+    RUTV_CK(cudaMemcpyAsync(h, L[0].w.pack, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RUTV_CK(cudaStreamSynchronize(st));
+    if (h[1] != 0.0) return RANDUTV_ERR_NONFINITE;
+    a_fro_ = std::sqrt(h[0]);
+  }
+
+  int64_t steps = 0, k_done = 0;
+  bool final_block = false;
+  int64_t r0f = 0, mif = 0, nif = 0, pf = 0;
+  std::vector<int64_t> nt(L.size()), c0(L.size());
+
+  for (int64_t i = 1; i <= s; ++i) {
+    const int64_t p = i - 1, r0 = b * p;
+    if (k_stop > 0 && r0 >= k_stop) break;
+    const int64_t mi = m - r0, ni = n - r0;
+    const int owner = int(p % P);
+    for (size_t l = 0; l < L.size(); ++l) {
+      c0[l] = b * blocks_before(p, L[l].r, P);
+      nt[l] = L[l].nl - c0[l];
+    }
+    if (b * i < m && b * i < n) {
+      const int64_t si = p;
+      // ---- sketch
+      set_gemm_role(C_GEMM_SKETCH);
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        gaussian_fill(st, lr.w.G, m, mi, b, seed, uint32_t(p), 0u);
+        dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.G, m, 0.0, lr.w.Y,
+           std::max<int64_t>(nt[l], 1));
+      }
+      for (int it = 0; it < q; ++it) {
+        if (reortho) {
+          set_gemm_role(C_GEMM_QR);
+          dist_gram_chol(&RankWork::Y, nt, 1);
+          double h[3];
+          RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+          RUTV_CK(cudaStreamSynchronize(st));
+          const bool ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
+          if (ok) {
+            for (size_t l = 0; l < L.size(); ++l) {
+              auto& lr = L[l];
+              dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
+                 lr.w.Y2, std::max<int64_t>(nt[l], 1));
+            }
+          } else {
+            int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr);
+            if (rc != OK) return rc;
+          }
+          for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
+          set_gemm_role(C_GEMM_SKETCH);
+        }
+        for (size_t l = 0; l < L.size(); ++l) {  // Z = X Y  (partial)
+          auto& lr = L[l];
+          dg(lr.w, st, false, false, mi, b, nt[l], 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
+             std::max<int64_t>(nt[l], 1), 0.0, lr.w.Z, mi);
+        }
+        comm.allreduce(bufs(&RankWork::Z), size_t(mi) * b, st);
+        for (size_t l = 0; l < L.size(); ++l) {  // Y = X^T Z
+          auto& lr = L[l];
+          dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Z, mi, 0.0,
+             lr.w.Y, std::max<int64_t>(nt[l], 1));
+        }
+      }
+      // ---- QR(Y) -> W_v (rows distributed), T_v
+      set_gemm_role(C_GEMM_QR);
+      std::vector<double*> Tv(L.size());
+      for (size_t l = 0; l < L.size(); ++l) Tv[l] = L[l].w.Tfin;  // T_v of this step
+      bool qr_ok = false;
+      if (o.qr_mode == 0) {
+        dist_gram_chol(&RankWork::Y, nt, 1);
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
+             lr.w.q1, std::max<int64_t>(nt[l], 1));
+        }
+        dist_gram_chol(&RankWork::q1, nt, 2);
+        // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, std::max<int64_t>(nt[l], 1), lr.w.pack, b);
+        }
+        comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
+        for (auto& lr : L) small_recon(st, b, lr.sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b);
+        qr_ok = read_int_sync(st, L[0].sw.flag) == 0;
+        if (qr_ok) {
+          for (size_t l = 0; l < L.size(); ++l) {
+            auto& lr = L[l];
+            if (nt[l] > 0)
+              dg(lr.w, st, false, false, nt[l], b, b, -1.0, lr.w.q1, nt[l], lr.sw.M, bp, 0.0, lr.w.Y, nt[l]);
+            if (lr.r == owner) small_put_unit_lower(st, b, lr.sw, lr.w.Y, std::max<int64_t>(nt[l], 1));
+          }
+        }
+      }
+      if (!qr_ok) {
+        int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 1, Tv.data());
+        if (rc != OK) return rc;
+        for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
+      }
+      // ---- right apply to all m rows
+      set_gemm_role(C_GEMM_RIGHT);
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        dg(lr.w, st, false, false, m, b, nt[l], 1.0, lr.T + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
+           std::max<int64_t>(nt[l], 1), 0.0, lr.w.P, m);
+      }
+      comm.allreduce(bufs(&RankWork::P), size_t(m) * b, st);
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        dg(lr.w, st, false, false, m, b, b, 1.0, lr.w.P, m, Tv[l], b, 0.0, lr.w.P2, m);
+        dg(lr.w, st, false, true, m, nt[l], b, -1.0, lr.w.P2, m, lr.w.Y, std::max<int64_t>(nt[l], 1), 1.0,
+           lr.T + c0[l] * lr.ldt, lr.ldt);
+      }
+      // ---- panel QR on the owner of block p, broadcast (W_u, T_u, R11)
+      const size_t wun = size_t(mi) * b;
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        if (lr.r != owner) continue;
+        double* X = lr.T + r0 + c0[l] * lr.ldt;
+        double* Wu = lr.w.pack;
+        copy_matrix(st, mi, b, X, lr.ldt, Wu, mi);
+        QrWork qw = lr.w.qw;
+        qw.mode = o.qr_mode;
+        qw.fallbacks = &fallbacks;
+        int rc = panel_qr(st, mi, b, Wu, mi, Wu + wun + size_t(b) * b, b, lr.w.tau, Wu + wun, b, qw);
+        if (rc != OK) return rc;
+        // T(I2,J2) = R11 (replaced by D after the SVD), T(I3,J2) = 0
+        copy_matrix(st, b, b, Wu + wun + size_t(b) * b, b, X, lr.ldt);
+        set_zero(st, mi - b, b, X + b, lr.ldt);
+      }
+      comm.bcast(bufs(&RankWork::pack), wun + 2 * size_t(b) * b, owner, st);
+      for (auto& lr : L)  // keep R11 for the deferred SVD
+        copy_matrix(st, b, b, lr.w.pack + wun + size_t(b) * b, b, lr.w.Rall + size_t(si) * b * b, b);
+      // ---- left apply to the local columns right of block p
+      set_gemm_role(C_GEMM_LEFT);
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        const int64_t cs = c0[l] + ((lr.r == owner) ? b : 0), nc = lr.nl - cs;
+        if (nc <= 0) continue;
+        double* Cm = lr.T + r0 + cs * lr.ldt;
+        const double* Wu = lr.w.pack;
+        dg(lr.w, st, true, false, nc, b, mi, 1.0, Cm, lr.ldt, Wu, mi, 0.0, lr.w.S, nc);
+        dg(lr.w, st, false, false, nc, b, b, 1.0, lr.w.S, nc, Wu + wun, b, 0.0, lr.w.S2, nc);
+        dg(lr.w, st, false, true, mi, nc, b, -1.0, Wu, mi, lr.w.S2, nc, 1.0, Cm, lr.ldt);
+      }
+      ++steps;
+      k_done = std::min(b * i, n);
+      if (o.tol > 0.0) {  // ||T(I3, J3)||_F over all ranks
+        const int64_t e2 = std::min(b * i, m);
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          const int64_t cs = c0[l] + ((lr.r == owner) ? b : 0), nc = lr.nl - cs;
+          fro2(st, m - e2, std::max<int64_t>(nc, 0), lr.T + e2 + cs * lr.ldt, lr.ldt, lr.w.nrm, lr.w.pack);
+        }
+        comm.allreduce(bufs(&RankWork::pack), 1, st);
+        double t2 = 0.0;
+        RUTV_CK(cudaMemcpyAsync(&t2, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
+        RUTV_CK(cudaStreamSynchronize(st));
+        if (std::sqrt(t2) <= o.tol * a_fro_) break;
+      }
+    } else {
+      // ---- final block on its owner: economical SVD of T(r0:m, r0:n)
+      final_block = true;
+      r0f = r0;
+      mif = mi;
+      nif = ni;
+      pf = p;
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        if (lr.r != owner) continue;
+        double* X = lr.T + r0 + c0[l] * lr.ldt;
+        if (mi > ni) {
+          double* Wf = lr.w.pack;
+          copy_matrix(st, mi, ni, X, lr.ldt, Wf, mi);
+          QrWork qw = lr.w.qw;
+          qw.mode = o.qr_mode;
+          qw.fallbacks = &fallbacks;
+          int rc = panel_qr(st, mi, ni, Wf, mi, lr.w.Rfin, ni, lr.w.tau, lr.w.Tfin, ni, qw);
+          if (rc != OK) return rc;
+        } else {
+          copy_matrix(st, ni, ni, X, lr.ldt, lr.w.Rfin, ni);
+        }
+      }
+      k_done = n;
+      break;
+    }
+  }
+
+  // ---- b x b SVDs (R11 on every rank: run redundantly) and folds
+  set_gemm_role(C_GEMM_OTHER);
+  for (auto& lr : L) {
+    if (steps > 0)
+      jacobi_svd_batched(st, (int)steps, (int)b, lr.w.Rall, b, b * b, lr.w.Dall, lr.w.Usall, lr.w.Vsall, lr.w.jwork,
+                         lr.w.sweeps);
+  }
+  for (int64_t si = 0; si < steps; ++si) {
+    const int64_t r0 = b * si;
+    const int owner = int(si % P);
+    for (size_t l = 0; l < L.size(); ++l) {
+      auto& lr = L[l];
+      const double* Us = lr.w.Usall + size_t(si) * b * b;
+      const double* Vs = lr.w.Vsall + size_t(si) * b * b;
+      const int64_t cb = b * blocks_before(si, lr.r, P);  // local offset of block si (if owned) / of J3
+      const int64_t cs = cb + ((lr.r == owner) ? b : 0), nc = lr.nl - cs;
+      if (nc > 0) {  // T(I2, J3) = Us^T T(I2, J3) on the local columns
+        dg(lr.w, st, true, false, b, nc, b, 1.0, Us, b, lr.T + r0 + cs * lr.ldt, lr.ldt, 0.0, lr.w.fold, b);
+        copy_matrix(st, b, nc, lr.w.fold, b, lr.T + r0 + cs * lr.ldt, lr.ldt);
+      }
+      if (lr.r == owner) {
+        write_diag_block(st, b, b, lr.w.Dall + si * b, lr.T + r0 + cb * lr.ldt, lr.ldt);
+        if (r0 > 0) {  // T(I1, J2) = T(I1, J2) Vs
+          dg(lr.w, st, false, false, r0, b, b, 1.0, lr.T + cb * lr.ldt, lr.ldt, Vs, b, 0.0, lr.w.fold, r0);
+          copy_matrix(st, r0, b, lr.w.fold, r0, lr.T + cb * lr.ldt, lr.ldt);
+        }
+      }
+    }
+  }
+  if (final_block) {
+    const int owner = int(pf % P);
+    for (auto& lr : L) {
+      if (lr.r != owner) continue;
+      const int64_t cb = b * blocks_before(pf, lr.r, P);
+      jacobi_svd_batched(st, 1, (int)nif, lr.w.Rfin, nif, nif * nif, lr.w.Dfin, lr.w.Usfin, lr.w.Vsfin, lr.w.jworkf,
+                         lr.w.sweeps + steps);
+      write_diag_block(st, mif, nif, lr.w.Dfin, lr.T + r0f + cb * lr.ldt, lr.ldt);
+      if (r0f > 0) {
+        dg(lr.w, st, false, false, r0f, nif, nif, 1.0, lr.T + cb * lr.ldt, lr.ldt, lr.w.Vsfin, nif, 0.0, lr.w.fold,
+           r0f);
+        copy_matrix(st, r0f, nif, lr.w.fold, r0f, lr.T + cb * lr.ldt, lr.ldt);
+      }
+    }
+  }
+
+  if (info) {
+    info->k_done = k_done;
+    info->steps = (int32_t)steps;
+    info->final_block = final_block ? 1 : 0;
+    info->a_fro = a_fro_;
+    info->qr_fallbacks = fallbacks;
+    info->max_sweeps = 0;
+    info->trailing_fro = 0.0;
+    if (k_done < n) {
+      for (size_t l = 0; l < L.size(); ++l) {
+        auto& lr = L[l];
+        const int64_t cs = b * blocks_before(cdiv(k_done, b), lr.r, P), nc = lr.nl - cs;
+        fro2(st, m - k_done, std::max<int64_t>(nc, 0), lr.T + k_done + cs * lr.ldt, lr.ldt, lr.w.nrm, lr.w.pack);
+      }
+      comm.allreduce(bufs(&RankWork::pack), 1, st);
+      double t2 = 0.0;
+      RUTV_CK(cudaMemcpyAsync(&t2, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
+      info->trailing_fro = std::sqrt(t2);
+    }
+    RUTV_CK(cudaStreamSynchronize(st));
+  }
+  return RANDUTV_OK;
+}
+
+std::mutex g_dmu;
+void* g_dws = nullptr;
+size_t g_dws_bytes = 0;
+
+void* dist_ws(size_t bytes) {
+  if (bytes > g_dws_bytes) {
+    if (g_dws) {
+      cudaDeviceSynchronize();
+      cudaFree(g_dws);
+      g_dws = nullptr;
+      g_dws_bytes = 0;
+    }
+    if (cudaMalloc(&g_dws, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      g_dws = nullptr;
+      return nullptr;
+    }
+    g_dws_bytes = bytes;
+  }
+  return g_dws;
+}
+
+}  // namespace
+}  // namespace rutv
+
+// ----------------------------------------------------------------------------- C ABI
+struct randutv_comm {
+  std::unique_ptr<rutv::Comm> c;
+};
+
+extern "C" {
+
+int randutv_nccl_unique_id(void* id_out) {
+  if (!id_out) return -1;
+  auto& api = rutv::nccl();
+  if (!api.ok) return RANDUTV_ERR_NCCL;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return RANDUTV_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == RANDUTV_NCCL_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(id_out, &id, sizeof(id));
+  return 0;
+}
+
+int randutv_comm_init_nccl(int32_t nranks, int32_t rank, const void* id, randutv_comm** out) {
+  if (nranks < 1) return -1;
+  if (rank < 0 || rank >= nranks) return -2;
+  if (!id) return -3;
+  if (!out) return -4;
+  if (!rutv::nccl().ok) return RANDUTV_ERR_NCCL;
+  try {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    auto* h = new randutv_comm;
+    h->c.reset(new rutv::NcclComm(nranks, rank, uid));
+    *out = h;
+    return 0;
+  } catch (const rutv::NcclError&) {
+    return RANDUTV_ERR_NCCL;
+  } catch (const rutv::CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+}
+
+int randutv_comm_init_loopback(int32_t nranks, randutv_comm** out) {
+  if (nranks < 1) return -1;
+  if (!out) return -2;
+  try {
+    auto* h = new randutv_comm;
+    h->c.reset(new rutv::LoopComm(nranks));
+    *out = h;
+    return 0;
+  } catch (const rutv::CudaError&) {
+    return RANDUTV_ERR_CUDA;
+  }
+}
+
+int randutv_comm_destroy(randutv_comm* c) {
+  delete c;
+  return 0;
+}
+
+int randutv_comm_local_ranks(const randutv_comm* c, int32_t* world, int32_t* ranks_out, int32_t max_ranks) {
+  if (!c) return -1;
+  if (world) *world = c->c->P;
+  const int nl = (int)c->c->ranks.size();
+  for (int i = 0; i < nl && i < max_ranks; ++i)
+    if (ranks_out) ranks_out[i] = c->c->ranks[i];
+  return nl;
+}
+
+int64_t randutv_dist_local_cols(int64_t n, int64_t b, int32_t rank, int32_t nranks) {
+  if (n < 0 || b < 1 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
+  return local_cols(n, b, rank, nranks);
+}
+
+int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_t rank, int32_t nranks) {
+  if (local_col < 0 || b < 1 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
+  const int64_t k = local_col / b, i = local_col % b;
+  return (k * nranks + rank) * b + i;
+}
+
+int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m, int64_t n, const double* const* A_loc,
+                        const int64_t* lda_loc, int64_t b, int32_t q, uint64_t seed, int64_t k_stop,
+                        double* const* T_loc, const int64_t* ldt_loc, randutv_info* info) {
+  if (!comm) return -2;
+  if (m < 1) return -3;
+  if (n < 1 || n > m) return -4;
+  if (!A_loc || !lda_loc) return -5;
+  if (b < 1 || b > RANDUTV_MAX_B) return -7;
+  if (q < 0) return -8;
+  if (k_stop < 0) return -10;
+  if (!T_loc || !ldt_loc) return -11;
+  randutv_opts o{};
+  if (opts) o = *opts;
+  if (o.tol < 0 || std::isnan(o.tol) || o.qr_mode < 0 || o.qr_mode > 1) return -1;
+  if (b > n) b = n;
+  rutv::Comm& c = *comm->c;
+  const int nlr = (int)c.ranks.size();
+  for (int l = 0; l < nlr; ++l) {
+    const int64_t nl = local_cols(n, b, c.ranks[l], c.P);
+    if (nl > 0 && (!A_loc[l] || lda_loc[l] < m)) return -5;
+    if (nl > 0 && (!T_loc[l] || ldt_loc[l] < m)) return -11;
+  }
+  std::lock_guard<std::mutex> lock(rutv::g_dmu);
+  try {
+    rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P);
+    const size_t per = rutv::dist_rank_bytes(d);
+    char* ws = (char*)rutv::dist_ws(per * nlr);
+    if (!ws) return RANDUTV_ERR_NOMEM;
+    std::vector<rutv::LocalRank> L(nlr);
+    for (int l = 0; l < nlr; ++l) {
+      auto& lr = L[l];
+      lr.r = c.ranks[l];
+      lr.A = A_loc[l];
+      lr.lda = lda_loc[l];
+      lr.T = T_loc[l];
+      lr.ldt = ldt_loc[l];
+      lr.nl = local_cols(n, b, lr.r, c.P);
+      rutv::Arena ar;
+      ar.base = ws + per * l;
+      ar.size = per;
+      lr.w = rutv::carve_rank(ar, d);
+      lr.w.qw.mode = o.qr_mode;
+      lr.sw = rutv::carve_small(lr.w.small, b);
+    }
+    rutv::DistFactor f(c, o, m, n, b, q, seed, k_stop, L);
+    return f.run(info);
+  } catch (const rutv::CudaError& e) {
+    fprintf(stderr, "randutv_factor_dist: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);
+    return RANDUTV_ERR_CUDA;
+  } catch (const rutv::NcclError& e) {
+    fprintf(stderr, "randutv_factor_dist: NCCL error %d\n", (int)e.r);
+    return RANDUTV_ERR_NCCL;
+  } catch (int code) {
+    return code;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+"""GPU parity of the multi-GPU algorithm (randutv_factor_dist) through the C
+ABI, on ONE GPU with the loopback communicator: P virtual ranks, each with its
+own block-cyclic shard, collectives as fixed-order device sums/copies between
+bulk-synchronous phases.  The assembled T must satisfy the same parity rule
+against the oracle as the single-GPU path (R18) and agree with the
+single-GPU factorization to rounding."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_1703_00998_b200 as P  # noqa: E402
+import testmat  # noqa: E402
+from paper_1703_00998_b200 import dist as D  # noqa: E402
+from util import EPS, check_parity, diag_blocks_ok  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(A):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(A).T)).cuda().t()
+
+
+def run_dist(A, nranks, b, q, seed, **kw):
+    m, n = A.shape
+    comm = D.loopback(nranks)
+    Ad = to_dev(A)
+    shards = [D.shard(Ad, b, r, nranks) for r in range(nranks)]
+    Ts, info = D.factor(comm, shards, m, n, b, q, seed, **kw)
+    torch.cuda.synchronize()
+    comm.close()
+    return D.assemble(Ts, n, min(b, n)).cpu().numpy(), info
+
+
+@pytest.mark.parametrize("name,scale,q,nranks", [
+    ("c1", 1.0, None, 2), ("c1", 1.0, None, 3), ("c2", 0.2, 2, 4), ("c3", 0.1, None, 2),
+    ("c3", 0.1, None, 8), ("c4", 0.05, None, 3)])
+def test_dist_loopback_parity(name, scale, q, nranks):
+    c = testmat.config(name, scale=scale, q=q)
+    A = c.A
+    m, n = A.shape
+    ref = oracle.randutv(A, c.b, c.q, c.seed, build_ortho=False)
+    T, info = run_dist(A, nranks, c.b, c.q, c.seed)
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert info.k_done == n and info.steps == ref["steps"]
+    assert np.all(np.tril(T, -1) == 0.0)
+    assert diag_blocks_ok(T, c.b, n)
+    assert abs(np.linalg.norm(T) - np.linalg.norm(A)) <= 4 * n * EPS * np.linalg.norm(A)
+    # the single-GPU path on the same input: equal to rounding
+    _, T1, _, _ = P.randutv(to_dev(A), c.b, c.q, c.seed, with_uv=False)
+    T1 = T1.cpu().numpy()
+    d1, dd = np.abs(np.diag(T1)), np.abs(np.diag(T))
+    assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * ref["a_fro"])
+
+
+def test_dist_one_rank_equals_single_gpu_bits():
+    """P = 1: the same kernels in the same order as randutv_factor_ex, except
+    that the Grams go through the packed allreduce buffer -- equal to rounding."""
+    c = testmat.config("c1", scale=0.4)
+    T, info = run_dist(c.A, 1, c.b, c.q, c.seed)
+    _, T1, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
+    np.testing.assert_allclose(np.abs(np.diag(T)), np.abs(np.diag(T1.cpu().numpy())), rtol=1e-12, atol=1e-13)
+
+
+def test_dist_more_ranks_than_blocks_and_ragged():
+    A = testmat.gaussian(333, 150, 11)
+    for nranks, b in ((4, 64), (5, 32), (3, 150)):
+        ref = oracle.randutv(A, b, 1, 5, build_ortho=False)
+        T, info = run_dist(A, nranks, b, 1, 5)
+        par = check_parity(T, ref["T"], ref["a_fro"])
+        assert par["diag_ok"] and par["ek_ok"], (nranks, b, par)
+
+
+def test_dist_early_stop_c5_like():
+    c = testmat.config("c5", scale=0.05)
+    ref = oracle.randutv(c.A, c.b, c.q, c.seed, k_stop=c.k_stop, tol=c.tol, build_ortho=False)
+    T, info = run_dist(c.A, 3, c.b, c.q, c.seed, k_stop=c.k_stop, tol=c.tol)
+    k = info.k_done
+    assert k == ref["k"] and info.steps == ref["steps"]
+    assert np.all(T[k:, :k] == 0)
+    np.testing.assert_allclose(np.abs(np.diag(T)[:k]), np.abs(np.diag(ref["T"])[:k]), rtol=1e-10,
+                               atol=c.A.shape[0] * EPS * ref["a_fro"])
+    assert abs(info.trailing_fro - ref["trailing_fro"]) <= 1e-8 * ref["trailing_fro"] + 1e3 * EPS * ref["a_fro"]
+
+
+def test_dist_householder_fallback_and_zero():
+    """qr_mode 1 forces the allgather + redundant Householder path; a zero
+    matrix triggers the CholeskyQR breakdown fallback in qr_mode 0."""
+    c = testmat.config("c2", scale=0.1)
+    ref = oracle.randutv(c.A, c.b, c.q, c.seed, build_ortho=False)
+    T, info = run_dist(c.A, 3, c.b, c.q, c.seed, qr_mode=1)
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    Z, info = run_dist(np.zeros((96, 96)), 2, 16, 1, 0)
+    assert np.all(Z == 0) and info.qr_fallbacks > 0
+
+
+def test_dist_nccl_one_rank():
+    """The NCCL communicator (unique id exchanged through torch.distributed,
+    symbols from the process's libnccl) on a 1-rank group."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29600 + os.getpid() % 500))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = D.nccl_from_torch()
+        assert comm.world == 1 and comm.ranks == [0]
+        c = testmat.config("c1", scale=0.4)
+        ref = oracle.randutv(c.A, c.b, c.q, c.seed, build_ortho=False)
+        Ts, info = D.factor(comm, [to_dev(c.A)], *c.A.shape, c.b, c.q, c.seed)
+        torch.cuda.synchronize()
+        par = check_parity(Ts[0].cpu().numpy(), ref["T"], ref["a_fro"])
+        assert par["diag_ok"] and par["ek_ok"], par
+        comm.close()
+    finally:
+        dist.destroy_process_group()
