@@ -19,8 +19,10 @@ def load(path):
     return data
 
 
-def summarize(path, top=25):
+def summarize(path, top=25, last=0):
     data = load(path)
+    if last:
+        data = data[-last:]
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
     tot, cnt, grid = collections.defaultdict(float), collections.Counter(), {}
     for d in data:
@@ -38,4 +40,5 @@ def summarize(path, top=25):
 
 
 if __name__ == "__main__":
-    print(summarize(sys.argv[1]))
+    last = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    print(summarize(sys.argv[1], last=last))
