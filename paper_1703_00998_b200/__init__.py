@@ -20,7 +20,7 @@ import numpy as np
 from . import flops  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_randutv.so")
+_LIB_PATH = os.environ.get("RANDUTV_LIB") or os.path.join(_HERE, "_randutv.so")
 _lib = None
 
 c_i64, c_i32, c_u64, c_u32, c_dbl, c_vp = (ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint32,

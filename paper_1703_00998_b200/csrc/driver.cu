@@ -156,17 +156,27 @@ void dg(const Work& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, 
 // Low-priority side stream per device for work off the critical path (the
 // deferred b x b SVDs): its kernels fill the SMs the latency-bound panel-QR
 // kernels leave idle, and the block scheduler prefers the main stream's CTAs.
-cudaStream_t side_stream() {
-  static cudaStream_t streams[64] = {};
+// which = 0: deferred SVD chunks; 1: trailing right-apply updates.
+cudaStream_t side_stream(int which = 0) {
+  static cudaStream_t streams[2][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) {
+  if (!streams[which][dev]) {
     int least = 0, greatest = 0;
     RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, least));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[which][dev], cudaStreamNonBlocking, least));
   }
-  return streams[dev];
+  return streams[which][dev];
+}
+
+// Two reusable events per device for the fork/join of the right-apply overlap.
+cudaEvent_t overlap_event(int which) {
+  static cudaEvent_t evs[2][64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
+  return evs[which][dev];
 }
 
 int check_qr(int rc) {
@@ -264,7 +274,19 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       double* TJ = T + r0 * m;
       dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
       dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
-      dg(w, st, false, true, m, ni, b, -1.0, w.P2, m, Wv, ldwv, 1.0, TJ, m);
+      // The panel QR below reads only the panel block T(r0:m, J2): update it
+      // first on the main stream; the rest of the rank-b update (columns J3 and
+      // the rows above the panel) runs on a low-priority side stream
+      // concurrently with the latency-bound panel QR, and the left apply waits
+      // for it.  Side GEMMs are unsplit (no shared split-K scratch).
+      dg(w, st, false, true, mi, b, b, -1.0, w.P2 + r0, m, Wv, ldwv, 1.0, X, m);
+      cudaStream_t upd = side_stream(1);
+      cudaEvent_t fork = overlap_event(0), join = overlap_event(1);
+      RUTV_CK(cudaEventRecord(fork, st));
+      RUTV_CK(cudaStreamWaitEvent(upd, fork, 0));
+      if (r0 > 0) dgemm(upd, false, true, r0, b, b, -1.0, w.P2, m, Wv, ldwv, 1.0, TJ, m, nullptr, 0);
+      dgemm(upd, false, true, m, ni - b, b, -1.0, w.P2, m, Wv + b, ldwv, 1.0, TJ + b * m, m, nullptr, 0);
+      RUTV_CK(cudaEventRecord(join, upd));
       // ---- U block: Householder QR of the panel T(r0:m, J2)
       double* Wu = w.Vu;
       int64_t ldwu = m;
@@ -279,7 +301,8 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       // T(I2,J2) = R11 (replaced by D after the batched SVD), T(I3,J2) = 0
       copy_matrix(st, b, b, R11, b, X, m);
       set_zero(st, mi - b, b, X + b, m);
-      // ---- left apply to T(r0:m, J3)
+      // ---- left apply to T(r0:m, J3), after the overlapped update
+      RUTV_CK(cudaStreamWaitEvent(st, join, 0));
       set_gemm_role(C_GEMM_LEFT);
       const int64_t nc = n - f2;
       double* Cm = T + r0 + f2 * m;
