@@ -222,6 +222,10 @@ RANDUTV_API long long randutv_launch_count(void);
 RANDUTV_API int randutv_profile_begin(void);
 RANDUTV_API int randutv_profile_end(double* ms, double* flops, long long* launches);
 RANDUTV_API const char* randutv_profile_class_name(int cls);
+/* Per-launch timeline of the last profile_begin/end window: 4 doubles per
+ * launch (class, stream slot numbered by first use, start ms, end ms relative
+ * to profile_begin).  Writes up to max_launches entries; returns the count. */
+RANDUTV_API long long randutv_profile_timeline(double* out, long long max_launches);
 
 #ifdef __cplusplus
 }

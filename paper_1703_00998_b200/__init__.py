@@ -85,6 +85,8 @@ def lib():
     L.randutv_profile_begin.restype = ctypes.c_int
     L.randutv_profile_end.argtypes = [c_vp, c_vp, c_vp]
     L.randutv_profile_end.restype = ctypes.c_int
+    L.randutv_profile_timeline.argtypes = [c_vp, ctypes.c_longlong]
+    L.randutv_profile_timeline.restype = ctypes.c_longlong
     L.randutv_profile_class_name.argtypes = [ctypes.c_int]
     L.randutv_profile_class_name.restype = ctypes.c_char_p
     for f in ("randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
@@ -97,7 +99,7 @@ def lib():
 EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
             "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
             "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
-            "randutv_profile_end", "randutv_profile_class_name", "randutv_nccl_unique_id",
+            "randutv_profile_end", "randutv_profile_class_name", "randutv_profile_timeline", "randutv_nccl_unique_id",
             "randutv_comm_init_nccl", "randutv_comm_init_loopback", "randutv_comm_destroy",
             "randutv_comm_local_ranks", "randutv_dist_local_cols", "randutv_dist_global_col",
             "randutv_factor_dist"]
@@ -125,6 +127,23 @@ def profile_end() -> dict:
         if name is None:
             break
         out[name.decode()] = {"ms": ms[i], "flops": fl[i], "launches": ln[i]}
+    return out
+
+
+def profile_timeline():
+    """Per-launch (class name, stream slot, start ms, end ms) of the last profile window."""
+    L = lib()
+    n = L.randutv_profile_timeline(None, 0)
+    buf = (ctypes.c_double * (4 * max(n, 1)))()
+    L.randutv_profile_timeline(buf, n)
+    names = {}
+    out = []
+    for i in range(n):
+        c = int(buf[4 * i])
+        if c not in names:
+            nm = L.randutv_profile_class_name(c)
+            names[c] = nm.decode() if nm else str(c)
+        out.append((names[c], int(buf[4 * i + 1]), buf[4 * i + 2], buf[4 * i + 3]))
     return out
 
 

@@ -75,6 +75,8 @@ struct Work {
   double *fold, *part, *nrm, *scal;
   int* flag;
   int* sweeps;
+  int* qflags;    // optimistic CholeskyQR decision flags
+  int qflags_cap;
   size_t part_elems;
   QrWork qw;
 };
@@ -125,6 +127,8 @@ Work carve(Arena& ar, const Plan& p) {
   w.scal = ar.take<double>(16);
   w.flag = ar.take<int>(16);
   w.sweeps = ar.take<int>(size_t(sb) + 16);
+  w.qflags_cap = int((p.q + 2) * std::max<int64_t>(p.nrand, 1) + 8);
+  w.qflags = ar.take<int>(size_t(w.qflags_cap));
   return w;
 }
 
@@ -185,9 +189,11 @@ int check_qr(int rc) {
 }
 
 // The factorization proper (device pointers only).
+constexpr int kRetry = 1000;  // factor_device: an optimistic CholeskyQR decision failed, redo synchronously
+
 int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
                   uint64_t seed, int64_t k_stop, double* U, double* T, double* V, randutv_info* info,
-                  void* ws, size_t ws_bytes) {
+                  void* ws, size_t ws_bytes, bool optimistic) {
   cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
   const bool uv = (U != nullptr);
   const bool reortho = (o.no_reortho == 0);
@@ -199,6 +205,12 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   int fallbacks = 0;
   w.qw.mode = o.qr_mode;
   w.qw.fallbacks = &fallbacks;
+  int nflags = 0;
+  if (optimistic && o.qr_mode == 0) {
+    w.qw.dev_flags = w.qflags;
+    w.qw.flag_count = &nflags;
+    w.qw.flag_cap = w.qflags_cap;
+  }
 
   // ---- T <- A, ||A||_F, non-finite scan (one host sync)
   RUTV_CK(cudaMemsetAsync(w.flag, 0, sizeof(int), st));
@@ -338,6 +350,17 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     }
   }
   if (!final_block && !stopped) k_done = std::min(k_done, n);
+  if (nflags > 0) {  // optimistic CholeskyQR decisions: one read for the whole loop
+    std::vector<int> hf(nflags);
+    RUTV_CK(cudaMemcpyAsync(hf.data(), w.qflags, sizeof(int) * nflags, cudaMemcpyDeviceToHost, st));
+    RUTV_CK(cudaStreamSynchronize(st));
+    for (int f : hf)
+      if (f) {
+        if (svd_side) RUTV_CK(cudaStreamSynchronize(side));
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+        return kRetry;
+      }
+  }
 
   set_gemm_role(C_GEMM_OTHER);
   // ---- batched small SVDs
@@ -557,7 +580,21 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     } else if (wsb < need) {
       return -12;
     }
-    if (!host) return factor_device(o, m, n, A, lda, b, q, seed, k_stop, U, T, V, info, ws, wsb);
+    // Optimistic first (no host synchronisation per panel QR); the synchronous
+    // per-panel fallback run only if a CholeskyQR decision failed.  Not when T
+    // aliases A (the first run would have destroyed the input).
+    auto overlaps = [&](const double* X, size_t xbytes) {
+      const char* a0 = (const char*)A;
+      const char* a1 = a0 + sizeof(double) * (size_t(lda) * (n - 1) + m);
+      const char* x0 = (const char*)X;
+      return x0 < a1 && a0 < x0 + xbytes;
+    };
+    const bool opt = !overlaps(T, sizeof(double) * size_t(m) * n);
+    if (!host) {
+      int rc2 = factor_device(o, m, n, A, lda, b, q, seed, k_stop, U, T, V, info, ws, wsb, opt);
+      if (rc2 == kRetry) rc2 = factor_device(o, m, n, A, lda, b, q, seed, k_stop, U, T, V, info, ws, wsb, false);
+      return rc2;
+    }
     // host buffers: stage through device memory inside the call
     const size_t elems = size_t(m) * n + (U ? size_t(m) * m + size_t(n) * n : 0);
     double* stage = (double*)cached_stage(elems * sizeof(double));
@@ -567,7 +604,12 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     double* dV = U ? dU + size_t(m) * m : nullptr;
     RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
                               cudaMemcpyDefault, st));
-    rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb);
+    rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, true);
+    if (rc == kRetry) {  // the input was factored in place: stage it again
+      RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
+                                cudaMemcpyDefault, st));
+      rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, false);
+    }
     if (rc == RANDUTV_OK) {
       RUTV_CK(cudaMemcpyAsync(T, dT, sizeof(double) * m * n, cudaMemcpyDefault, st));
       if (U) {
@@ -617,6 +659,15 @@ int randutv_profile_end(double* ms, double* flops, long long* launches) {
     if (launches) launches[i] = i < K_NCLASS ? c4[i] : 0;
   }
   return 0;
+}
+
+long long randutv_profile_timeline(double* out, long long max_launches) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const std::vector<double>& tl = prof_timeline();
+  const long long n = (long long)(tl.size() / 4);
+  if (out)
+    for (long long i = 0; i < std::min(n, max_launches) * 4; ++i) out[i] = tl[size_t(i)];
+  return n;
 }
 
 const char* randutv_profile_class_name(int cls) {

@@ -347,11 +347,19 @@ jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict
   }
 }
 
+constexpr int MAX_CLUSTER = 8;
+
 JacobiDesc make_desc(int k) {
   JacobiDesc d;
-  // 2 kb columns of B and W in shared memory: 32 kb k bytes <= ~200 KB
+  // 2 kb columns of B and W in shared memory: 32 kb k bytes <= ~200 KB.  One
+  // warp rotates one column pair per sub-round; a sub-round's latency grows
+  // with the warps contending for the FP64 pipe, while the number of
+  // sequential sub-rounds per sweep (~2k) does not depend on kb, so prefer
+  // narrow blocks (kb = 8: 8 warps) as long as the matrix fits one cluster.
   int kb = 16;
   while (kb > 1 && size_t(32) * kb * k > 200 * 1024) kb /= 2;
+  // (kb = 8 on a 16-CTA cluster for k = 256 was measured: 25 % lower latency
+  // per matrix but 2x the SMs per matrix -- slower overall as a side stream)
   d.k = k;
   d.kb = kb;
   d.nb = (int)cdiv(k, kb);
@@ -363,7 +371,7 @@ JacobiDesc make_desc(int k) {
 
 bool jacobi_single_launch(int k) {
   JacobiDesc d = make_desc(k);
-  return k > 1 && d.nb / 2 <= 8;
+  return k > 1 && d.nb / 2 <= MAX_CLUSTER;
 }
 
 size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 1); }
@@ -383,16 +391,17 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
   const double tol = double(k) * DBL_EPSILON;
   const int csize = d.nb / 2;
-  if (k > 1 && csize <= 8) {
+  if (k > 1 && csize <= MAX_CLUSTER) {
     // one cluster per matrix runs every round and sweep in-kernel
     static size_t attr_c = 0;
     if (smem > attr_c) {
       RUTV_CK(cudaFuncSetAttribute(jacobi_cluster_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      RUTV_CK(cudaFuncSetAttribute(jacobi_cluster_k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       attr_c = smem;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize, batch, 1);
-    cfg.blockDim = dim3(JNT, 1, 1);
+    cfg.blockDim = dim3(32 * d.kb, 1, 1);  // one warp per column pair of a block pair
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

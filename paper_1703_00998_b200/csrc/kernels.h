@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 namespace rutv {
 
@@ -36,6 +37,9 @@ struct ProfScope {
 };
 void prof_begin();
 void prof_end(double* ms, double* flops, long long* counts);
+// per-launch timeline of the last profile: 4 doubles per launch
+// (class, stream slot in order of first use, start ms, end ms from prof_begin)
+const std::vector<double>& prof_timeline();
 
 // ---- gemm.cu -------------------------------------------------------------
 // C = alpha op(A) op(B) + beta C.  ``part`` (part_elems doubles) is the split-K
@@ -100,7 +104,16 @@ struct QrWork {
   double* small = nullptr;  // small_work_elems(b) doubles
   int mode = 0;             // 0: CholeskyQR2 + reconstruction, Householder fallback; 1: Householder only
   int* fallbacks = nullptr; // host counter of fallbacks taken (may be null)
+  // Optimistic mode (no host synchronisation): the CholeskyQR results are used
+  // unconditionally and each decision flag goes to dev_flags[*flag_count]++;
+  // the caller checks them once at the end and redoes the factorization in the
+  // synchronous mode if any is raised.
+  int* dev_flags = nullptr;
+  int* flag_count = nullptr;  // host counter (slots used)
+  int flag_cap = 0;
 };
+// writes flag = (stats[0] != 0 || stats[2] > kappa_max * stats[1]) (CholeskyQR re-orthonormalization test)
+void reortho_flag(cudaStream_t st, const double* stats, double kappa_max, int* flag);
 size_t qr_work_elems(int64_t b);
 // Q = thin orthonormal basis of span(Y) with Y = Q R, R upper triangular (the
 // re-orthonormalisation of the power loop, R5): CholeskyQR when the

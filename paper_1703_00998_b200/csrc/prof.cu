@@ -16,7 +16,11 @@ struct Rec {
   int cls;
   cudaEvent_t a, b;
   double flops;
+  cudaStream_t st;
 };
+cudaEvent_t g_t0 = nullptr;  // timeline origin (recorded at prof_begin on the legacy stream)
+std::vector<double> g_tl;     // [cls, stream slot, start ms, end ms] per launch of the last profile
+std::vector<cudaStream_t> g_streams;
 bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
@@ -63,14 +67,19 @@ ProfScope::~ProfScope() {
   if (!g_on || !a_) return;
   cudaEvent_t b = take_event();
   cudaEventRecord(b, st_);
-  g_recs.push_back(Rec{cls_, (cudaEvent_t)a_, b, flops_});
+  g_recs.push_back(Rec{cls_, (cudaEvent_t)a_, b, flops_, st_});
 }
 
 void prof_begin() {
   g_on = true;
   g_recs.clear();
   g_pool_used = 0;
+  RUTV_CK(cudaDeviceSynchronize());
+  if (!g_t0) RUTV_CK(cudaEventCreate(&g_t0));
+  RUTV_CK(cudaEventRecord(g_t0, 0));
 }
+
+const std::vector<double>& prof_timeline() { return g_tl; }
 
 void prof_end(double* ms, double* flops, long long* counts) {
   RUTV_CK(cudaDeviceSynchronize());
@@ -79,12 +88,19 @@ void prof_end(double* ms, double* flops, long long* counts) {
     flops[c] = 0.0;
     counts[c] = 0;
   }
+  g_tl.clear();
+  g_streams.clear();
   for (auto& r : g_recs) {
-    float t = 0.f;
+    float t = 0.f, t0 = 0.f;
     RUTV_CK(cudaEventElapsedTime(&t, r.a, r.b));
+    RUTV_CK(cudaEventElapsedTime(&t0, g_t0, r.a));
     ms[r.cls] += t;
     flops[r.cls] += r.flops;
     counts[r.cls] += 1;
+    size_t slot = 0;
+    while (slot < g_streams.size() && g_streams[slot] != r.st) ++slot;
+    if (slot == g_streams.size()) g_streams.push_back(r.st);
+    g_tl.insert(g_tl.end(), {double(r.cls), double(slot), double(t0), double(t0 + t)});
   }
   g_on = false;
   g_recs.clear();

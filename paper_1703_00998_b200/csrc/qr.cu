@@ -412,6 +412,19 @@ __global__ void zero_lower_k(int64_t b, double* R, int64_t ldr) {
 }
 }  // namespace
 
+namespace {
+__global__ void reortho_flag_k(const double* stats, double kappa_max, int* flag) {
+  if (threadIdx.x == 0) *flag = !(stats[0] == 0.0 && stats[2] <= kappa_max * stats[1]);
+}
+}  // namespace
+
+void reortho_flag(cudaStream_t st, const double* stats, double kappa_max, int* flag) {
+  ProfScope _p(st, K_MISC, 0.0);
+  count_launch(K_MISC);
+  reortho_flag_k<<<1, 32, 0, st>>>(stats, kappa_max, flag);
+  RUTV_LAUNCH_CK();
+}
+
 int qr_max_rows() { return QR_MAX_CLUSTER * QR_NT * 16; }
 
 size_t qr_work_elems(int64_t b) { return size_t(3) * 32 * size_t(b) + 1024; }
@@ -497,8 +510,10 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
     dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems);     // Q1
     dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems);      // G2
+    const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
+    if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
     small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt);
-    if (read_flag_sync(st, sw.flag) == 0) {
+    if (optimistic || read_flag_sync(st, sw.flag) == 0) {
       if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
         dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems);
       small_put_unit_lower(st, b, sw, V, ldv);
@@ -517,11 +532,19 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
     const int bp = sw.bp;
     dgemm(st, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, bp, w.part, w.part_elems);
     small_chol_inv(st, b, sw);
-    double h[3];
-    read_stats_sync(st, sw.stats, h);
     // kappa(R1) estimated by its diagonal: CholeskyQR's loss of orthogonality
     // ~ kappa^2 eps stays <= 1e-8 -- ample for a basis of the power loop
-    if (h[0] == 0.0 && h[2] <= 1e4 * h[1]) {
+    constexpr double kKappaMax = 1e4;
+    bool ok;
+    if (w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap) {
+      reortho_flag(st, sw.stats, kKappaMax, w.dev_flags + (*w.flag_count)++);
+      ok = true;
+    } else {
+      double h[3];
+      read_stats_sync(st, sw.stats, h);
+      ok = h[0] == 0.0 && h[2] <= kKappaMax * h[1];
+    }
+    if (ok) {
       dgemm(st, false, false, m, b, b, 1.0, Y, ldy, sw.R1i, bp, 0.0, Q, ldq, w.part, w.part_elems);
       return OK;
     }
