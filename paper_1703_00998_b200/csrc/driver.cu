@@ -232,6 +232,11 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   cudaStream_t side = svd_side ? side_stream() : nullptr;
   int64_t svd_done = 0;
   std::vector<cudaEvent_t> evs;
+  struct SvdChunk {
+    int64_t s0, s1;
+    cudaEvent_t done;
+  };
+  std::vector<SvdChunk> chunks;
   auto launch_svd_chunk = [&]() {
     if (steps <= svd_done) return;
     cudaEvent_t e;
@@ -243,6 +248,11 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     jacobi_svd_batched(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, w.Dall + s0 * b,
                        w.Usall + size_t(s0) * b * b, w.Vsall + size_t(s0) * b * b,
                        w.jwork + jacobi_work_elems((int)s0, (int)b), w.sweeps + s0);
+    cudaEvent_t done;
+    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    evs.push_back(done);
+    RUTV_CK(cudaEventRecord(done, side));
+    chunks.push_back({s0, steps, done});
     svd_done = steps;
   };
   int64_t r0f = 0, nif = 0, mif = 0;
@@ -367,23 +377,20 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   int max_sweeps = 0;
   if (svd_side) {
     launch_svd_chunk();
-    if (!evs.empty()) {
-      cudaEvent_t e;
-      RUTV_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      evs.push_back(e);
-      RUTV_CK(cudaEventRecord(e, side));
-      RUTV_CK(cudaStreamWaitEvent(st, e, 0));
-    }
-    for (cudaEvent_t e : evs) cudaEventDestroy(e);
   } else if (steps > 0) {
     jacobi_svd_batched(st, (int)steps, (int)b, w.Rall, b, b * b, w.Dall, w.Usall, w.Vsall, w.jwork, w.sweeps);
+    chunks.push_back({0, steps, nullptr});
   }
   if (final_block)
     jacobi_svd_batched(st, 1, (int)nif, w.Rfin, nif, nif * nif, w.Dfin, w.Usfin, w.Vsfin, w.jworkf,
                        w.sweeps + steps);
 
-  // ---- folds into T (deferred)
-  for (int64_t si = 0; si < steps; ++si) {
+  // ---- folds into T (deferred), chunk by chunk as the side-stream
+  // SVDs complete (all folds stay on the main stream: left and right products
+  // commute, so their order does not matter, but they must not run concurrently)
+  for (const SvdChunk& ch : chunks) {
+    if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
+  for (int64_t si = ch.s0; si < ch.s1; ++si) {
     const int64_t r0 = b * si;
     const double* Us = w.Usall + size_t(si) * b * b;
     const double* Vs = w.Vsall + size_t(si) * b * b;
@@ -398,6 +405,8 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       copy_matrix(st, r0, b, w.fold, r0, T + r0 * m, m);
     }
   }
+  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
   if (final_block) {
     write_diag_block(st, mif, nif, w.Dfin, T + r0f + r0f * m, m);               // [diag(D); 0]
     if (r0f > 0) {
