@@ -30,6 +30,7 @@ from __future__ import annotations
 import math
 
 import numpy as np
+import scipy.linalg
 
 from .householder import apply_left_t, apply_right, geqr2, larft, thin_q, unit_lower
 from .philox import gaussian_block
@@ -37,7 +38,7 @@ from .small_svd import small_svd
 
 
 def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
-            reortho: bool = True, build_ortho: bool = True, gaussian=None, record: bool = False):
+            reortho: bool = True, build_ortho: bool = True, gaussian=None, record: bool = False, p: int = 0):
     """Factor A (m x n, m >= n) as U T V^T.
 
     Parameters follow the C-ABI ``randutv_factor`` (include/randutv.h):
@@ -46,7 +47,11 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
     (reading R11); ``reortho`` re-orthonormalizes Y before every X Y (R5);
     ``build_ortho`` = False returns U = V = None (the paper's "no orthonormal
     matrices" mode, PAPER.md:1204-1206, 1630-1631).  ``gaussian(step, rows, cols)``
-    overrides the Philox draw (tests only).
+    overrides the Philox draw (tests only).  ``p`` > 0 over-samples the sketch
+    (Remark remark:positivep; Fig. fig:stepUTVoversampling,
+    PAPER.md:1754-1765): G gets b + p_i columns, p_i = min(p, n_i - b) (reading
+    R23), and QR(Y) is replaced by QR of the b dominant left singular vectors of
+    the extended Y.
 
     Returns a dict with U, T, V, k (columns processed), steps (randomized
     steps taken), trailing_fro = ||T(k+1:m, k+1:n)||_F and a_fro = ||A||_F.
@@ -55,8 +60,8 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
     m, n = A.shape
     if m < n:
         raise ValueError("m < n is not supported (fat final step is out of scope, R8)")
-    if b < 1 or q < 0 or k_stop < 0:
-        raise ValueError("invalid b, q or k_stop")
+    if b < 1 or q < 0 or k_stop < 0 or p < 0:
+        raise ValueError("invalid b, q, k_stop or p")
     if not np.all(np.isfinite(A)):
         raise ValueError("non-finite input")
     if gaussian is None:
@@ -81,12 +86,16 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
         J3_nonempty = b * i < n
         if I3_nonempty and J3_nonempty:
             X = T[r0:, r0:]                                   # X = T([I2,I3],[J2,J3])
-            G = gaussian(i - 1, m - r0, b)                    # P:941 (R1: m_i x b)
+            p_i = min(p, (n - r0) - b)                        # R23 (p = 0: the paper's Fig. fig:randUTV)
+            G = gaussian(i - 1, m - r0, b + p_i)              # P:941 (R1: m_i x b), P:1131 (m x (b+p))
             Y = X.T @ G
             for _ in range(q):
                 if reortho:
                     Y = thin_q(Y)
                 Y = X.T @ (X @ Y)
+            if p_i > 0:                                       # [Z,~,~] = svd(Y,'econ')
+                Z = scipy.linalg.svd(Y, full_matrices=False, lapack_driver="gesvd")[0]
+                Y = np.asfortranarray(Z[:, :b])               # qr(Z(:,1:b))
             Fv, tau_v = geqr2(Y)
             Vv = unit_lower(Fv, b)
             Tv = larft(Vv, tau_v)

@@ -23,21 +23,27 @@ from util import EPS, diag_blocks_ok, ek_fro, invariants
 
 
 # ----------------------------------------------------------------------------- brute force
-def simplistic_randutv(A, b, q, seed, reortho=True):
+def simplistic_randutv(A, b, q, seed, reortho=True, p=0):
     """Fig. fig:randUTVmatlab with dense unitary matrices (O(n^4)); stepUTV's
-    ``svd(A*V(:,1:b))`` realised as QR + small SVD (Remark rem:econ_svd)."""
+    ``svd(A*V(:,1:b))`` realised as QR + small SVD (Remark rem:econ_svd).
+    p > 0: stepUTV of Fig. fig:stepUTVoversampling,
+    ``[Z,~,~] = svd(Y,'econ'); [V,~] = qr(Z(:,1:b))`` with numpy's SVD (LAPACK
+    gesdd, not the oracle's gesvd), p_i = min(p, n_i - b) (reading R23)."""
     m, n = A.shape
     T = A.copy(); U = np.eye(m); V = np.eye(n)
     for i in range(1, math.ceil(n / b) + 1):
         r0 = b * (i - 1)
         Ai = T[r0:, r0:]
         if Ai.shape[1] > b:
-            G = gaussian_block(seed, i - 1, Ai.shape[0], b)
+            p_i = min(p, Ai.shape[1] - b)
+            G = gaussian_block(seed, i - 1, Ai.shape[0], b + p_i)
             Y = Ai.T @ G
             for _ in range(q):
                 if reortho:
                     Y = np.linalg.qr(Y)[0]
                 Y = Ai.T @ (Ai @ Y)
+            if p_i > 0:
+                Y = np.linalg.svd(Y, full_matrices=False)[0][:, :b]
             VV = np.linalg.qr(Y, mode="complete")[0]
             UU, R = np.linalg.qr(Ai @ VV[:, :b], mode="complete")
             Us, D, W = small_svd(R[:b, :b])
@@ -75,6 +81,43 @@ def test_efficient_equals_simplistic(m, n, b, q):
     np.testing.assert_allclose(r["T"], T2, atol=1e-11 * a)
     np.testing.assert_allclose(r["U"], U2, atol=1e-10)
     np.testing.assert_allclose(r["V"], V2, atol=1e-10)
+
+
+@pytest.mark.parametrize("m,n,b,q,p", [(48, 48, 8, 1, 5), (60, 45, 8, 2, 8), (40, 33, 10, 0, 3)])
+def test_oversampling_efficient_equals_simplistic(m, n, b, q, p):
+    """Over-sampled randUTV (Remark remark:positivep) vs the dense transcription
+    of Fig. fig:stepUTVoversampling: Z's column signs are free (LAPACK gesvd vs
+    gesdd), which flips signs of T's rows/columns but not |diag T| nor e_k."""
+    A = testmat.gaussian(m, n, seed=m + n + p)
+    r = randutv(A, b, q, seed=9, p=p)
+    U2, T2, V2 = simplistic_randutv(A, b, q, seed=9, p=p)
+    a = np.linalg.norm(A)
+    np.testing.assert_allclose(np.abs(np.diag(r["T"])), np.abs(np.diag(T2)), rtol=1e-10, atol=1e-13 * a)
+    np.testing.assert_allclose(ek_fro(r["T"]), ek_fro(T2), rtol=1e-10, atol=1e-13 * a)
+    np.testing.assert_allclose(np.abs(r["T"]), np.abs(T2), atol=1e-11 * a)
+    inv = invariants(A, r["U"], r["T"], r["V"])
+    assert inv["recon"] < 1e-14 * n and inv["orth_u"] < 1e-13 * n and inv["orth_v"] < 1e-13 * n
+    # p = 0 is the paper's Fig. fig:randUTV exactly
+    r0 = randutv(A, b, q, seed=9, p=0)
+    r1 = randutv(A, b, q, seed=9)
+    assert np.array_equal(r0["T"], r1["T"])
+
+
+def test_oversampling_improves_first_block():
+    """Remark remark:positivep / App. app:oversampling: over-sampling aligns
+    col(V_1) better with the dominant right singular vectors, so the first
+    block's D (= sigma(A V_1) <= sigma_j, interlacing) moves towards sigma."""
+    m = n = 200
+    b = 20
+    rng = np.random.default_rng(5)
+    s = 0.95 ** np.arange(n)
+    A = (np.linalg.qr(rng.standard_normal((m, n)))[0] * s) @ np.linalg.qr(rng.standard_normal((n, n)))[0].T
+    gaps = []
+    for p in (0, 10):
+        d = np.mean([np.sum(s[:b] - np.diag(randutv(A, b, 0, seed=t, k_stop=b, p=p, build_ortho=False)["T"])[:b])
+                     for t in range(6)])
+        gaps.append(d)
+    assert gaps[1] < gaps[0]
 
 
 # ----------------------------------------------------------------------------- Theorem §5.3
