@@ -56,7 +56,14 @@ typedef struct randutv_opts {
                              reconstruction, column-by-column Householder as the fallback
                              for ill-conditioned panels (R20); 1: Householder only */
   void* workspace;        /* optional caller device workspace (NULL: library cache)        */
-  size_t workspace_bytes; /* its size; must be >= randutv_workspace_size(...)              */
+  size_t workspace_bytes; /* its size; must be >= randutv_workspace_size_ex(...)           */
+  int32_t oversample;     /* p >= 0: over-sampled sketch (Remark remark:positivep,
+                             PAPER.md:1124-1142; Fig. fig:stepUTVoversampling): G has
+                             b + p_i columns, p_i = min(p, n_i - b), and QR(Y) acts on the
+                             b dominant left singular vectors of the extended Y.  0 = the
+                             paper's Fig. fig:randUTV.  b + p <= RANDUTV_MAX_B.  Single-GPU
+                             entry points only (randutv_factor_dist: RANDUTV_ERR_UNSUPPORTED) */
+  int32_t reserved1;
 } randutv_opts;
 
 /* Diagnostics filled by randutv_factor_ex (may be NULL). */
@@ -110,6 +117,9 @@ RANDUTV_API int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n
 /* Device workspace bytes randutv_factor_ex needs for this shape
  * (with_uv != 0: U and V requested). */
 RANDUTV_API size_t randutv_workspace_size(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv);
+/* The same with over-sampling p (randutv_opts.oversample). */
+RANDUTV_API size_t randutv_workspace_size_ex(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv,
+                                             int32_t oversample);
 
 RANDUTV_API const char* randutv_strerror(int code);
 RANDUTV_API const char* randutv_version(void);

@@ -36,7 +36,8 @@ class RandUTVError(RuntimeError):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("stream", c_vp), ("tol", c_dbl), ("no_reortho", c_i32), ("qr_mode", c_i32),
-                ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t), ("oversample", c_i32),
+                ("reserved1", c_i32)]
 
 
 class _Info(ctypes.Structure):
@@ -71,6 +72,8 @@ def lib():
     L.randutv_factor.restype = ctypes.c_int
     L.randutv_workspace_size.argtypes = [c_i64, c_i64, c_i64, c_i32, c_i32]
     L.randutv_workspace_size.restype = ctypes.c_size_t
+    L.randutv_workspace_size_ex.argtypes = [c_i64, c_i64, c_i64, c_i32, c_i32, c_i32]
+    L.randutv_workspace_size_ex.restype = ctypes.c_size_t
     L.randutv_strerror.argtypes = [ctypes.c_int]
     L.randutv_strerror.restype = ctypes.c_char_p
     L.randutv_version.restype = ctypes.c_char_p
@@ -96,7 +99,8 @@ def lib():
     return L
 
 
-EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_strerror",
+EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "randutv_workspace_size_ex",
+            "randutv_strerror",
             "randutv_version", "randutv_gaussian", "randutv_dgemm", "randutv_panel_qr", "randutv_panel_qr_ex",
             "randutv_small_svd_batched", "randutv_launch_count", "randutv_profile_begin",
             "randutv_profile_end", "randutv_profile_class_name", "randutv_profile_timeline", "randutv_nccl_unique_id",
@@ -189,7 +193,7 @@ def _check(rc: int, where: str):
 
 # --------------------------------------------------------------------------- the factorization
 def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reortho: bool = True,
-            with_uv: bool = True, stream=None, out=None, qr_mode: int = 0):
+            with_uv: bool = True, stream=None, out=None, qr_mode: int = 0, oversample: int = 0):
     """A = U T V^T (Fig. fig:randUTV) on the GPU.
 
     ``A``: torch CUDA tensor (m x n, m >= n) or a numpy array (host buffers,
@@ -199,7 +203,7 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
     """
     L = lib()
     if isinstance(A, np.ndarray):
-        return _randutv_host(A, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode)
+        return _randutv_host(A, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode, oversample)
     torch = _torch()
     A = as_colmajor(A)
     m, n = A.shape
@@ -210,7 +214,7 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
         U = empty_cm(m, m, A.device) if with_uv else None
         V = empty_cm(n, n, A.device) if with_uv else None
     opts = _Opts(stream=_stream(stream, A.device).value, tol=float(tol), no_reortho=0 if reortho else 1,
-                 qr_mode=int(qr_mode))
+                 qr_mode=int(qr_mode), oversample=int(oversample))
     info = _Info()
     rc = L.randutv_factor_ex(ctypes.byref(opts), m, n, A.data_ptr(), _ld(A), int(b), int(q), int(seed) & (2**64 - 1),
                              int(k_stop), U.data_ptr() if U is not None else None, T.data_ptr(),
@@ -221,14 +225,15 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0, reo
                          info.a_fro, info.qr_fallbacks)
 
 
-def _randutv_host(A: np.ndarray, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode=0):
+def _randutv_host(A: np.ndarray, b, q, seed, k_stop, tol, reortho, with_uv, qr_mode=0, oversample=0):
     L = lib()
     A = np.asfortranarray(A, dtype=np.float64)
     m, n = A.shape
     T = np.empty((m, n), order="F")
     U = np.empty((m, m), order="F") if with_uv else None
     V = np.empty((n, n), order="F") if with_uv else None
-    opts = _Opts(stream=None, tol=float(tol), no_reortho=0 if reortho else 1, qr_mode=int(qr_mode))
+    opts = _Opts(stream=None, tol=float(tol), no_reortho=0 if reortho else 1, qr_mode=int(qr_mode),
+                 oversample=int(oversample))
     info = _Info()
     p = lambda X: X.ctypes.data if X is not None else None  # noqa: E731
     rc = L.randutv_factor_ex(ctypes.byref(opts), m, n, p(A), m, int(b), int(q), int(seed) & (2**64 - 1),

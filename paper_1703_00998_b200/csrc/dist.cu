@@ -806,7 +806,8 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   if (!T_loc || !ldt_loc) return -11;
   randutv_opts o{};
   if (opts) o = *opts;
-  if (o.tol < 0 || std::isnan(o.tol) || o.qr_mode < 0 || o.qr_mode > 1) return -1;
+  if (o.tol < 0 || std::isnan(o.tol) || o.qr_mode < 0 || o.qr_mode > 1 || o.oversample < 0) return -1;
+  if (o.oversample > 0) return RANDUTV_ERR_UNSUPPORTED;  // over-sampling: single-GPU path only
   if (b > n) b = n;
   rutv::Comm& c = *comm->c;
   const int nlr = (int)c.ranks.size();

@@ -39,6 +39,7 @@ size_t g_stage_bytes = 0;
 
 struct Plan {
   int64_t m, n, b;
+  int64_t ovs = 0;    // over-sampling p (Remark remark:positivep); sketch width bs = b + p
   int q;
   bool uv;
   int64_t s;          // loop bound min(ceil(m/b), ceil(n/b))
@@ -48,9 +49,9 @@ struct Plan {
   size_t elems_v = 0, elems_u = 0;
 };
 
-Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv) {
+Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv, int64_t ovs = 0) {
   Plan p;
-  p.m = m; p.n = n; p.b = b; p.q = q; p.uv = uv;
+  p.m = m; p.n = n; p.b = b; p.q = q; p.uv = uv; p.ovs = ovs;
   p.s = std::min(cdiv(m, b), cdiv(n, b));
   p.nrand = 0;
   for (int64_t i = 1; i <= p.s; ++i)
@@ -69,6 +70,7 @@ Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv) {
 
 struct Work {
   double *G, *Y, *Y2, *P, *P2, *Vu, *Wt, *Wt2, *tau, *Rtmp, *Ttmp;
+  double *Qo, *Ro, *Do, *Uso, *Vso, *jworko;  // over-sampling: thin Q, R, SVD of R (width b + p)
   double *Tv, *Tu, *Rall, *Dall, *Usall, *Vsall, *jwork;
   double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf;
   double *Wv_all, *Wu_all;
@@ -85,17 +87,26 @@ Work carve(Arena& ar, const Plan& p) {
   Work w{};
   const int64_t m = p.m, n = p.n, b = p.b, mx = std::max(m, n);
   const int64_t sb = std::max<int64_t>(p.nrand, 1);
-  w.G = ar.take<double>(size_t(m) * b);
-  w.Y = ar.take<double>(size_t(n) * b);
-  w.Y2 = ar.take<double>(size_t(n) * b);
+  const int64_t bs = b + p.ovs;  // sketch width
+  w.G = ar.take<double>(size_t(m) * bs);
+  w.Y = ar.take<double>(size_t(n) * bs);
+  w.Y2 = ar.take<double>(size_t(n) * bs);
+  if (p.ovs > 0) {
+    w.Qo = ar.take<double>(size_t(n) * bs);
+    w.Ro = ar.take<double>(size_t(bs) * bs);
+    w.Do = ar.take<double>(size_t(bs));
+    w.Uso = ar.take<double>(size_t(bs) * bs);
+    w.Vso = ar.take<double>(size_t(bs) * bs);
+    w.jworko = ar.take<double>(jacobi_work_elems(1, (int)bs));
+  }
   w.P = ar.take<double>(size_t(m) * b);
   w.P2 = ar.take<double>(size_t(m) * b);
   w.Vu = ar.take<double>(size_t(m) * b);
   w.Wt = ar.take<double>(size_t(n) * b);
   w.Wt2 = ar.take<double>(size_t(n) * b);
-  w.tau = ar.take<double>(size_t(b));
-  w.Rtmp = ar.take<double>(size_t(b) * b);
-  w.Ttmp = ar.take<double>(size_t(b) * b);
+  w.tau = ar.take<double>(size_t(bs));
+  w.Rtmp = ar.take<double>(size_t(bs) * bs);
+  w.Ttmp = ar.take<double>(size_t(bs) * bs);
   w.Tv = ar.take<double>(size_t(sb) * b * b);
   w.Tu = ar.take<double>(size_t(sb + 1) * b * b);
   w.Rall = ar.take<double>(size_t(sb) * b * b);
@@ -113,16 +124,16 @@ Work carve(Arena& ar, const Plan& p) {
     w.Wu_all = ar.take<double>(p.elems_u);
   }
   w.fold = ar.take<double>(size_t(mx) * b);
-  w.part_elems = size_t(8) * mx * b + size_t(148) * 32 * 1024;
+  w.part_elems = size_t(8) * mx * bs + size_t(148) * 32 * 1024;
   w.part = ar.take<double>(w.part_elems);
   w.qw.part = w.part;
   w.qw.part_elems = w.part_elems;
-  w.qw.sfull = ar.take<double>(size_t(32) * b);
-  w.qw.s2 = ar.take<double>(size_t(32) * b);
-  w.qw.z = ar.take<double>(size_t(32) * b);
-  w.qw.q1_elems = size_t(mx) * b;
+  w.qw.sfull = ar.take<double>(size_t(32) * bs);
+  w.qw.s2 = ar.take<double>(size_t(32) * bs);
+  w.qw.z = ar.take<double>(size_t(32) * bs);
+  w.qw.q1_elems = size_t(mx) * bs;
   w.qw.q1 = ar.take<double>(w.qw.q1_elems);
-  w.qw.small = ar.take<double>(small_work_elems(b));
+  w.qw.small = ar.take<double>(small_work_elems(bs));
   w.nrm = ar.take<double>(8192);
   w.scal = ar.take<double>(16);
   w.flag = ar.take<int>(16);
@@ -197,7 +208,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
   const bool uv = (U != nullptr);
   const bool reortho = (o.no_reortho == 0);
-  Plan p = make_plan(m, n, b, q, uv);
+  Plan p = make_plan(m, n, b, q, uv, o.oversample);
   Arena ar;
   ar.base = (char*)ws;
   ar.size = ws_bytes;
@@ -269,17 +280,30 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       const int64_t si = i - 1;  // 0-based step slot
       // ---- sketch
       set_gemm_role(C_GEMM_SKETCH);
-      gaussian_fill(st, w.G, m, mi, b, seed, uint32_t(i - 1), 0u);
-      dg(w, st, true, false, ni, b, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
+      const int64_t p_i = std::min<int64_t>(p.ovs, ni - b);  // over-sampling (R23); 0 = Fig. fig:randUTV
+      const int64_t bw = b + p_i;                            // sketch width
+      gaussian_fill(st, w.G, m, mi, bw, seed, uint32_t(i - 1), 0u);
+      dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
       double* Ycur = w.Y;
       double* Yalt = w.Y2;
       for (int it = 0; it < q; ++it) {
         if (reortho) {
-          check_qr(rutv::reortho(st, ni, b, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, w.qw));
+          check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, w.qw));
           std::swap(Ycur, Yalt);
         }
-        dg(w, st, false, false, mi, b, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);       // Z = X Y
-        dg(w, st, true, false, ni, b, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);        // Y = X^T Z
+        dg(w, st, false, false, mi, bw, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);      // Z = X Y
+        dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);       // Y = X^T Z
+      }
+      if (p_i > 0) {
+        // Y <- the b dominant left singular vectors of the extended Y (P:1133-1135,
+        // Fig. fig:stepUTVoversampling ``[Z,~,~] = svd(Y,'econ')``): Y = Q R,
+        // R = Us D Vs^T, Z = Q Us(:, 1:b).  Column signs of Z are free (R9/A.3).
+        GemmRole role(C_GEMM_QR);
+        check_qr(panel_qr(st, ni, bw, Ycur, n, w.Ro, bw, w.tau, w.Ttmp, bw, w.qw));
+        thin_q(st, ni, bw, Ycur, n, w.Ttmp, bw, w.Qo, n, w.Rtmp, w.part, w.part_elems);
+        jacobi_svd_batched(st, 1, (int)bw, w.Ro, bw, bw * bw, w.Do, w.Uso, w.Vso, w.jworko, nullptr);
+        dg(w, st, false, false, ni, b, bw, 1.0, w.Qo, n, w.Uso, bw, 0.0, Yalt, n);
+        std::swap(Ycur, Yalt);
       }
       // ---- V block: Householder QR of Y
       double* Wv = Ycur;
@@ -559,9 +583,13 @@ const char* randutv_strerror(int code) {
 }
 
 size_t randutv_workspace_size(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv) {
-  if (m < 1 || n < 1 || b < 1) return 0;
+  return randutv_workspace_size_ex(m, n, b, q, with_uv, 0);
+}
+
+size_t randutv_workspace_size_ex(int64_t m, int64_t n, int64_t b, int32_t q, int32_t with_uv, int32_t oversample) {
+  if (m < 1 || n < 1 || b < 1 || oversample < 0) return 0;
   b = std::min<int64_t>(b, std::max(m, n));
-  return workspace_bytes(make_plan(m, n, b, q, with_uv != 0));
+  return workspace_bytes(make_plan(m, n, b, q, with_uv != 0, oversample));
 }
 
 int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
@@ -573,13 +601,14 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
   if (opts) o = *opts;
   if (o.tol < 0 || std::isnan(o.tol)) return -12;
   if (o.qr_mode < 0 || o.qr_mode > 1) return -12;
+  if (o.oversample < 0 || b + o.oversample > RANDUTV_MAX_B) return -12;
   if (b > n) b = n;  // a single final-SVD step, same result as any b >= n
   std::lock_guard<std::mutex> lock(g_mu);
   try {
     const bool host = mem_kind(A) == MEM_HOST || mem_kind(T) == MEM_HOST || (U && mem_kind(U) == MEM_HOST) ||
                       (V && mem_kind(V) == MEM_HOST);
     cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
-    const size_t need = workspace_bytes(make_plan(m, n, b, q, U != nullptr));
+    const size_t need = workspace_bytes(make_plan(m, n, b, q, U != nullptr, o.oversample));
     void* ws = o.workspace;
     size_t wsb = o.workspace_bytes;
     if (!ws) {

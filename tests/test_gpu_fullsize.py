@@ -95,6 +95,25 @@ def test_c3_full():
     assert np.all(d[3000:] >= 0.9 * c.sigma[3000:]) and np.all(d[3000:] <= 1.3 * c.sigma[3000:])
 
 
+def test_c3_full_oversampled_first_step():
+    """Over-sampling p = 10 at the c3 size: the first block against the oracle
+    run with k_stop = b on the same bytes (R23: 2 decades per block keep the
+    selection of Y's dominant directions well posed)."""
+    A, c = device_case("c3")
+    m, n = A.shape
+    T = P.empty_cm(m, n)
+    _, T, _, info = P.randutv(A, c.b, c.q, c.seed, k_stop=c.b, with_uv=False, out=(None, T, None), oversample=10)
+    torch.cuda.synchronize()
+    Ah = np.asfortranarray(A.cpu().numpy())
+    ref = oracle.randutv(Ah, c.b, c.q, c.seed, k_stop=c.b, build_ortho=False, p=10)
+    b = c.b
+    floor = n * EPS * ref["a_fro"]
+    d_gpu = torch.diagonal(T[:b, :b]).abs().cpu().numpy()
+    d_ref = np.abs(np.diag(ref["T"])[:b])
+    assert np.all(np.abs(d_gpu - d_ref) <= 1e-10 * d_ref + floor), np.max(np.abs(d_gpu - d_ref) / d_ref)
+    assert abs(info.trailing_fro - ref["trailing_fro"]) <= 1e-8 * ref["trailing_fro"] + floor
+
+
 def test_c4_full_tall():
     A, c = device_case("c4")
     T, info = factor_T(A, c)

@@ -250,3 +250,36 @@ def test_deterministic():
     _, T1, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
     _, T2, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
     assert torch.equal(T1, T2)
+
+
+# ----------------------------------------------------------------------------- over-sampling (NEXT row 1)
+@pytest.mark.parametrize("name,scale,q,p,uv", [("c1", 1.0, None, 5, True), ("c2", 0.2, 1, 10, False),
+                                                ("c2", 0.3, 2, 7, False), ("c4", 0.05, None, 3, True)])
+def test_randutv_oversampling_parity(name, scale, q, p, uv):
+    """Remark remark:positivep / Fig. fig:stepUTVoversampling on the GPU (QR of the
+    extended Y, Jacobi SVD of its R factor, Z = Q Us(:, 1:b)) vs the oracle's
+    LAPACK-SVD transcription; R23 caps p_i = min(p, n_i - b).  Parity needs the
+    selection of the b dominant directions of Y' to be well posed
+    (sigma_b(Y') / sigma_1(Y') >> eps, R23): spectra decaying by <= ~2 decades
+    per block (c1, c2, c4; full-size c3 in test_gpu_fullsize)."""
+    c = testmat.config(name, scale=scale, q=q)
+    A = c.A
+    m, n = A.shape
+    ref = oracle.randutv(A, c.b, c.q, c.seed, build_ortho=uv, p=p)
+    U, T, V, info = P.randutv(to_dev(A), c.b, c.q, c.seed, with_uv=uv, oversample=p)
+    torch.cuda.synchronize()
+    Th = to_host(T)
+    par = check_parity(Th, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert np.all(np.tril(Th, -1) == 0.0) and diag_blocks_ok(Th, c.b, n)
+    if uv:
+        inv = invariants(A, to_host(U), Th, to_host(V))
+        assert inv["recon"] <= 1e-13 * n and inv["orth_u"] <= 1e-13 * n and inv["orth_v"] <= 1e-13 * n
+
+
+def test_oversampling_argument_checks():
+    A = to_dev(testmat.gaussian(64, 64, 1))
+    with pytest.raises(P.RandUTVError):
+        P.randutv(A, 16, 1, 0, oversample=-1)
+    with pytest.raises(P.RandUTVError):
+        P.randutv(A, 256, 1, 0, oversample=300)     # b + p > RANDUTV_MAX_B
