@@ -58,8 +58,6 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
     """
     A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
-    if m < n:
-        raise ValueError("m < n is not supported (fat final step is out of scope, R8)")
     if b < 1 or q < 0 or k_stop < 0 or p < 0:
         raise ValueError("invalid b, q, k_stop or p")
     if not np.all(np.isfinite(A)):
@@ -129,6 +127,26 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
         else:
             X = T[r0:, r0:]
             mi, ni = X.shape
+            if mi < ni:                                       # fat: Remark "The case m < n"
+                # unpivoted QR of the ROWS: X^T = Q [Rf; 0], Rf = Ur D Vr^T, so
+                # X = Vr D (Q blockdiag(Ur, I))^T[:mi, :]: U_small = Vr and
+                # V_small = Q blockdiag(Ur, I), a product of Householder reflectors
+                Ff, tau_f = geqr2(X.T)
+                Vf = unit_lower(Ff, mi)
+                Tf = larft(Vf, tau_f)
+                Ur, D, Vr = small_svd(np.triu(Ff[:mi, :mi]))
+                if build_ortho:
+                    U[:, r0:] = U[:, r0:] @ Vr
+                    V[:, r0:] = apply_right(V[:, r0:], Vf, Tf)
+                    V[:, r0:r0 + mi] = V[:, r0:r0 + mi] @ Ur
+                T[:r0, r0:] = apply_right(T[:r0, r0:], Vf, Tf)
+                T[:r0, r0:r0 + mi] = T[:r0, r0:r0 + mi] @ Ur
+                T[r0:, r0:] = 0.0
+                T[r0 + np.arange(mi), r0 + np.arange(mi)] = D
+                k_done = m
+                if record:
+                    log.append({"step": i, "final": True, "D": D})
+                break
             if mi > ni:                                       # tall: Remark rem:econ_svd
                 Ff, tau_f = geqr2(X)
                 Vf = unit_lower(Ff, ni)
@@ -149,7 +167,7 @@ def randutv(A, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
             k_done = n
             if record:
                 log.append({"step": i, "final": True, "D": D})
-    trailing = float(np.linalg.norm(T[k_done:, k_done:])) if k_done < n else 0.0
+    trailing = float(np.linalg.norm(T[k_done:, k_done:])) if k_done < min(m, n) else 0.0
     out = {"U": U, "T": T, "V": V, "k": k_done, "steps": steps, "trailing_fro": trailing,
            "a_fro": a_fro}
     if record:

@@ -31,10 +31,10 @@ def simplistic_randutv(A, b, q, seed, reortho=True, p=0):
     gesdd, not the oracle's gesvd), p_i = min(p, n_i - b) (reading R23)."""
     m, n = A.shape
     T = A.copy(); U = np.eye(m); V = np.eye(n)
-    for i in range(1, math.ceil(n / b) + 1):
+    for i in range(1, math.ceil(min(m, n) / b) + 1):
         r0 = b * (i - 1)
         Ai = T[r0:, r0:]
-        if Ai.shape[1] > b:
+        if Ai.shape[0] > b and Ai.shape[1] > b:
             p_i = min(p, Ai.shape[1] - b)
             G = gaussian_block(seed, i - 1, Ai.shape[0], b + p_i)
             Y = Ai.T @ G
@@ -57,8 +57,8 @@ def simplistic_randutv(A, b, q, seed, reortho=True, p=0):
             UU, s, Vh = np.linalg.svd(Ai, full_matrices=True)
             VV = Vh.T.copy()
             k = len(s)                                      # same canonical sign as small_svd
-            sg = np.sign(VV[np.argmax(np.abs(VV), axis=0), np.arange(k)])
-            VV *= sg[None, :]
+            sg = np.sign(VV[np.argmax(np.abs(VV[:, :k]), axis=0), np.arange(k)])
+            VV[:, :k] *= sg[None, :]
             UU[:, :k] *= sg[None, :]
             TT = np.zeros_like(Ai)
             TT[np.arange(len(s)), np.arange(len(s))] = s
@@ -81,6 +81,33 @@ def test_efficient_equals_simplistic(m, n, b, q):
     np.testing.assert_allclose(r["T"], T2, atol=1e-11 * a)
     np.testing.assert_allclose(r["U"], U2, atol=1e-10)
     np.testing.assert_allclose(r["V"], V2, atol=1e-10)
+
+
+@pytest.mark.parametrize("m,n,b,q", [(33, 48, 8, 1), (20, 50, 8, 2), (40, 41, 10, 0), (16, 40, 8, 1)])
+def test_fat_efficient_equals_simplistic(m, n, b, q):
+    """m < n (Remark "The case m < n"): the final fat block by a QR of
+    its rows; the dense transcription takes a full LAPACK SVD of that block."""
+    A = testmat.gaussian(m, n, seed=m * n)
+    r = randutv(A, b, q, seed=4)
+    U2, T2, V2 = simplistic_randutv(A, b, q, seed=4)
+    a = np.linalg.norm(A)
+    np.testing.assert_allclose(np.abs(np.diag(r["T"])), np.abs(np.diag(T2)), rtol=1e-10, atol=1e-13 * a)
+    np.testing.assert_allclose(ek_fro(r["T"]), ek_fro(T2), rtol=1e-10, atol=1e-13 * a)
+    inv = invariants(A, r["U"], r["T"], r["V"])
+    assert inv["recon"] < 1e-14 * n and inv["orth_u"] < 1e-13 * n and inv["orth_v"] < 1e-13 * n
+    assert inv["tril_max"] == 0.0 and r["k"] == m
+
+
+def test_fat_b_geq_m_is_svd():
+    """b >= m: a single final step = the SVD of A (textbook), T = [diag(sigma) 0]."""
+    A = testmat.gaussian(12, 30, 8)
+    r = randutv(A, b=16, q=1, seed=0)
+    T = r["T"]
+    np.testing.assert_allclose(np.diag(T), np.linalg.svd(A, compute_uv=False), rtol=1e-13)
+    off = T.copy(); off[np.arange(12), np.arange(12)] = 0
+    assert np.all(off == 0)
+    inv = invariants(A, r["U"], T, r["V"])
+    assert inv["recon"] < 1e-14 * 30 and inv["orth_v"] < 1e-13 * 30
 
 
 @pytest.mark.parametrize("m,n,b,q,p", [(48, 48, 8, 1, 5), (60, 45, 8, 2, 8), (40, 33, 10, 0, 3)])
@@ -267,7 +294,7 @@ def test_reortho_invariance_and_determinism():
 
 def test_errors():
     with pytest.raises(ValueError):
-        randutv(np.ones((3, 5)), 2, 1, 0)
+        randutv(np.ones((3, 5)), 0, 1, 0)
     with pytest.raises(ValueError):
         randutv(np.full((4, 4), np.nan), 2, 1, 0)
     with pytest.raises(ValueError):
