@@ -81,8 +81,10 @@ typedef struct randutv_info {
 /*
  * randutv_factor -- A = U T V^T  (Fig. fig:randUTV).
  *
- *  1 m, 2 n    sizes, 1 <= n <= m (the fat case m < n, is not
- *              built: returns -2)
+ *  1 m, 2 n    sizes >= 1.  m < n (fat) follows the Remark "The case m < n"
+ *              (PAPER.md:905-915): the final block is reduced by a QR of its rows
+ *              and then k_done = m (single-GPU entry points; randutv_factor_dist
+ *              needs n <= m)
  *  3 A         m x n input, leading dimension 4 lda >= m.  Read only.  Host or
  *              device memory.  May alias T when lda == m (in-place).
  *  5 b         block size, 1 <= b <= RANDUTV_MAX_B

@@ -235,7 +235,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   const double a_fro = std::sqrt(a2);
 
   int64_t steps = 0, k_done = 0;
-  bool final_block = false, final_tall = false;
+  bool final_block = false, final_tall = false, final_fat = false;
   // The b x b SVDs of R11 are independent of later steps (R13): with
   // the single-cluster Jacobi kernel they run in chunks on the side stream.
   constexpr int64_t kSvdChunk = 8;
@@ -376,14 +376,23 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         int64_t ldwf = uv ? mi : m;
         copy_matrix(st, mi, ni, X, m, Wf, ldwf);
         check_qr(panel_qr(st, mi, ni, Wf, ldwf, w.Rfin, ni, w.tau, w.Tu + size_t(p.nrand) * b * b, ni, w.qw));
+      } else if (mi < ni) {
+        // fat (Remark "The case m < n"): unpivoted QR of the ROWS,
+        // X^T = Q [Rf; 0]; with Rf = Ur D Vr^T: X = Vr [D 0] (Q blockdiag(Ur, I))^T
+        final_fat = true;
+        double* Wf = uv ? (w.Wv_all + p.off_v[i - 1]) : w.Wt;
+        int64_t ldwf = uv ? ni : n;
+        transpose_matrix(st, mi, ni, X, m, Wf, ldwf);
+        check_qr(panel_qr(st, ni, mi, Wf, ldwf, w.Rfin, mi, w.tau, w.Tu + size_t(p.nrand) * b * b, mi, w.qw));
       } else {
         copy_matrix(st, ni, ni, X, m, w.Rfin, ni);
       }
-      k_done = n;
+      k_done = std::min(m, n);
       break;
     }
   }
-  if (!final_block && !stopped) k_done = std::min(k_done, n);
+  if (!final_block && !stopped) k_done = std::min(k_done, std::min(m, n));
+  const int64_t kf = std::min(mif, nif);  // order of the final block's SVD
   if (nflags > 0) {  // optimistic CholeskyQR decisions: one read for the whole loop
     std::vector<int> hf(nflags);
     RUTV_CK(cudaMemcpyAsync(hf.data(), w.qflags, sizeof(int) * nflags, cudaMemcpyDeviceToHost, st));
@@ -406,8 +415,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     chunks.push_back({0, steps, nullptr});
   }
   if (final_block)
-    jacobi_svd_batched(st, 1, (int)nif, w.Rfin, nif, nif * nif, w.Dfin, w.Usfin, w.Vsfin, w.jworkf,
-                       w.sweeps + steps);
+    jacobi_svd_batched(st, 1, (int)kf, w.Rfin, kf, kf * kf, w.Dfin, w.Usfin, w.Vsfin, w.jworkf, w.sweeps + steps);
 
   // ---- folds into T (deferred), chunk by chunk as the side-stream
   // SVDs complete (all folds stay on the main stream: left and right products
@@ -431,7 +439,22 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   }
   }
   for (cudaEvent_t e : evs) cudaEventDestroy(e);
-  if (final_block) {
+  if (final_block && final_fat) {
+    // T(I2, J) = [diag(D) 0];  T(I1, J) <- T(I1, J) Q blockdiag(Ur, I)
+    write_diag_block(st, mif, mif, w.Dfin, T + r0f + r0f * m, m);
+    set_zero(st, mif, nif - mif, T + r0f + (r0f + mif) * m, m);
+    if (r0f > 0) {
+      const double* Wf = uv ? (w.Wv_all + p.off_v[p.s - 1]) : w.Wt;
+      const int64_t ldwf = uv ? nif : n;
+      const double* Tf = w.Tu + size_t(p.nrand) * b * b;
+      double* TJ = T + r0f * m;
+      dg(w, st, false, false, r0f, mif, nif, 1.0, TJ, m, Wf, ldwf, 0.0, w.P, r0f);
+      dg(w, st, false, false, r0f, mif, mif, 1.0, w.P, r0f, Tf, mif, 0.0, w.P2, r0f);
+      dg(w, st, false, true, r0f, nif, mif, -1.0, w.P2, r0f, Wf, ldwf, 1.0, TJ, m);
+      dg(w, st, false, false, r0f, mif, mif, 1.0, TJ, m, w.Usfin, mif, 0.0, w.fold, r0f);
+      copy_matrix(st, r0f, mif, w.fold, r0f, TJ, m);
+    }
+  } else if (final_block) {
     write_diag_block(st, mif, nif, w.Dfin, T + r0f + r0f * m, m);               // [diag(D); 0]
     if (r0f > 0) {
       dg(w, st, false, false, r0f, nif, nif, 1.0, T + r0f * m, m, w.Vsfin, nif, 0.0, w.fold, r0f);
@@ -450,6 +473,14 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       dg(w, st, true, false, nif, mif, mif, 1.0, Wf, mif, Ub, m, 0.0, w.fold, nif);   // Wf^T U'
       dg(w, st, false, false, nif, mif, nif, 1.0, Tf, nif, w.fold, nif, 0.0, w.P, nif);  // Tf (.)
       dg(w, st, false, false, mif, mif, nif, -1.0, Wf, mif, w.P, nif, 1.0, Ub, m);      // U' -= Wf (.)
+    }
+    if (final_block && final_fat) {  // V' <- Q V' with Q = I - Wf Tf Wf^T (ni x ni, mi reflectors)
+      const double* Wf = w.Wv_all + p.off_v[p.s - 1];
+      const double* Tf = w.Tu + size_t(p.nrand) * b * b;
+      double* Vb = V + r0f + r0f * n;
+      dg(w, st, true, false, mif, nif, nif, 1.0, Wf, nif, Vb, n, 0.0, w.fold, mif);
+      dg(w, st, false, false, mif, nif, mif, 1.0, Tf, mif, w.fold, mif, 0.0, w.Wt2, mif);
+      dg(w, st, false, false, nif, nif, mif, -1.0, Wf, nif, w.Wt2, mif, 1.0, Vb, n);
     }
     for (int64_t si = steps - 1; si >= 0; --si) {
       const int64_t r0 = b * si, mi = m - r0, ni = n - r0;
@@ -476,11 +507,13 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       dg(w, st, false, false, n, b, b, 1.0, V + r0 * n, n, w.Vsall + size_t(si) * b * b, b, 0.0, w.fold, n);
       copy_matrix(st, n, b, w.fold, n, V + r0 * n, n);
     }
-    if (final_block) {
-      dg(w, st, false, false, m, nif, nif, 1.0, U + r0f * m, m, w.Usfin, nif, 0.0, w.fold, m);
-      copy_matrix(st, m, nif, w.fold, m, U + r0f * m, m);
-      dg(w, st, false, false, n, nif, nif, 1.0, V + r0f * n, n, w.Vsfin, nif, 0.0, w.fold, n);
-      copy_matrix(st, n, nif, w.fold, n, V + r0f * n, n);
+    if (final_block) {  // fat: U_small = Vr, V_small = Q blockdiag(Ur, I)
+      const double* Uf = final_fat ? w.Vsfin : w.Usfin;
+      const double* Vf = final_fat ? w.Usfin : w.Vsfin;
+      dg(w, st, false, false, m, kf, kf, 1.0, U + r0f * m, m, Uf, kf, 0.0, w.fold, m);
+      copy_matrix(st, m, kf, w.fold, m, U + r0f * m, m);
+      dg(w, st, false, false, n, kf, kf, 1.0, V + r0f * n, n, Vf, kf, 0.0, w.fold, n);
+      copy_matrix(st, n, kf, w.fold, n, V + r0f * n, n);
     }
   }
 
@@ -551,7 +584,7 @@ void* cached_stage(size_t bytes) {
 int validate(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, int64_t k_stop, double* U,
              double* T, double* V) {
   if (m < 1) return -1;
-  if (n < 1 || n > m) return -2;
+  if (n < 1) return -2;
   if (!A) return -3;
   if (lda < m) return -4;
   if (b < 1 || b > RANDUTV_MAX_B) return -5;
@@ -602,7 +635,7 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
   if (o.tol < 0 || std::isnan(o.tol)) return -12;
   if (o.qr_mode < 0 || o.qr_mode > 1) return -12;
   if (o.oversample < 0 || b + o.oversample > RANDUTV_MAX_B) return -12;
-  if (b > n) b = n;  // a single final-SVD step, same result as any b >= n
+  if (b > std::min(m, n)) b = std::min(m, n);  // a single final-SVD step, same result as any larger b
   std::lock_guard<std::mutex> lock(g_mu);
   try {
     const bool host = mem_kind(A) == MEM_HOST || mem_kind(T) == MEM_HOST || (U && mem_kind(U) == MEM_HOST) ||

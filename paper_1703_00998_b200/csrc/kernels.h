@@ -57,6 +57,8 @@ int gemm_choose_splits(int64_t M, int64_t N, int64_t K, size_t part_elems);
 void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc);
 void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd);
 void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd);  // D = I (m x n)
+// D (n x m) = S^T for an m x n S
+void transpose_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd);
 void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd);
 // Copy S -> D (may alias when equal), accumulate sum of squares and a
 // non-finite flag.  out2[0] = ||S||_F^2 (deterministic two-pass), flag[0] != 0 if any

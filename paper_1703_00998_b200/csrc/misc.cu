@@ -28,6 +28,22 @@ __global__ void copy_k(int64_t m, int64_t n, const double* __restrict__ S, int64
       D[i + j * ldd] = S[i + j * lds];
 }
 
+// D (n x m) = S^T (S m x n); 32x32 smem tiles, coalesced both ways
+__global__ void transpose_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds, double* __restrict__ D,
+                            int64_t ldd) {
+  __shared__ double t[32][33];
+  const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    t[r][threadIdx.x] = (i < m && j < n) ? S[i + j * lds] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;  // D(j, i) = S(i, j)
+    if (i < m && j < n) D[j + i * ldd] = t[threadIdx.x][r];
+  }
+}
+
 __global__ void ident_k(int64_t m, int64_t n, double* D, int64_t ldd, double diagv) {
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
@@ -104,6 +120,13 @@ void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C,
 void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0 || S == D) return;
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); copy_k<<<grid2(m, n), TB, 0, st>>>(m, n, S, lds, D, ldd); }
+  RUTV_LAUNCH_CK();
+}
+
+void transpose_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
+  if (m <= 0 || n <= 0) return;
+  dim3 g((unsigned)cdiv(m, 32), (unsigned)cdiv(n, 32));
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); transpose_k<<<g, dim3(32, 8), 0, st>>>(m, n, S, lds, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 

@@ -40,7 +40,7 @@ def test_workspace_size_monotone():
 
 
 @pytest.mark.parametrize("args,code", [
-    (dict(m=0), -1), (dict(n=0), -2), (dict(n=6), -2), (dict(A=None), -3), (dict(lda=3), -4),
+    (dict(m=0), -1), (dict(n=0), -2), (dict(A=None), -3), (dict(lda=3), -4),
     (dict(b=0), -5), (dict(b=2000), -5), (dict(q=-1), -6), (dict(k_stop=-1), -8),
     (dict(U=None), -9), (dict(T=None), -10),
 ])

@@ -283,3 +283,24 @@ def test_oversampling_argument_checks():
         P.randutv(A, 16, 1, 0, oversample=-1)
     with pytest.raises(P.RandUTVError):
         P.randutv(A, 256, 1, 0, oversample=300)     # b + p > RANDUTV_MAX_B
+
+
+# ----------------------------------------------------------------------------- fat inputs (NEXT row 2)
+@pytest.mark.parametrize("m,n,b,q,uv", [(300, 500, 50, 1, True), (400, 1000, 64, 1, False), (130, 400, 32, 2, True),
+                                        (100, 333, 128, 1, True), (256, 300, 50, 1, False)])
+def test_randutv_fat_parity(m, n, b, q, uv):
+    """m < n (Remark "The case m < n"): the randomized steps as for
+    m >= n, the final fat block by a QR of its rows (transpose + panel QR), its
+    triangular factor's SVD, and V's last factor = the row reflectors."""
+    A = testmat.gaussian(m, n, m + n)
+    ref = oracle.randutv(A, b, q, 7, build_ortho=uv)
+    U, T, V, info = P.randutv(to_dev(A), b, q, 7, with_uv=uv)
+    torch.cuda.synchronize()
+    Th = to_host(T)
+    par = check_parity(Th, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert info.k_done == m and info.final_block and np.all(np.tril(Th, -1) == 0.0)
+    assert np.all(Th[:, m:][np.arange(m) >= (m // b) * b if m % b else np.zeros(m, bool)] == 0)
+    if uv:
+        inv = invariants(A, to_host(U), Th, to_host(V))
+        assert inv["recon"] <= 1e-13 * n and inv["orth_u"] <= 1e-13 * n and inv["orth_v"] <= 1e-13 * n
