@@ -22,6 +22,7 @@ householder unpivoted Householder QR (LAPACK dlarfg convention, reading R3),
             forward compact-WY T factor, right/left applications
 small_svd   b x b SVD via LAPACK gesvd
 randutv     the blocked driver of Fig. fig:randUTV
+rsvd        the randomized SVD of Remark remark:RSVD
 
 Pins (``tests/test_oracle_*.py``): cuRAND's host Philox, LAPACK dgeqrf, the
 explicit reflector product, closed forms, the dense Fig. ``fig:randUTVmatlab``
@@ -33,3 +34,4 @@ from .philox import philox4x32_10, uniforms, gaussian_block  # noqa: F401
 from .householder import house, geqr2, larft, unit_lower, apply_right, apply_left_t, thin_q  # noqa: F401
 from .small_svd import small_svd  # noqa: F401
 from .randutv import randutv  # noqa: F401
+from .rsvd import rsvd  # noqa: F401
