@@ -167,6 +167,19 @@ RANDUTV_API int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv
 RANDUTV_API int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,
                               double* Us, double* Vs, int32_t* sweeps, void* stream);
 
+/* Randomized SVD (Remark remark:RSVD; NEXT row 3 of
+ * SURVEY.md §8(f)): A (m x n, device, ld lda) ~ U diag(D) V^T with U (m x b,
+ * ld ldu) and V (n x b, ld ldv) orthonormal, D (b, non-increasing) -- device
+ * outputs.  G is the step-0 Philox draw of randutv_factor (m x (b+p),
+ * p = opts->oversample); Y = (A^T A)^q A^T G with opts->no_reortho honoured;
+ * Q = orth(Y) by the panel QR (opts->qr_mode); B = A Q = Q_B R_B; R_B = Us D Vs^T;
+ * U = Q_B Us(:,1:b), V = Q Vs(:,1:b).  Requires b + p <= min(m, n) and
+ * <= RANDUTV_MAX_B.  Asynchronous on opts->stream except for the panel QRs'
+ * fallback decisions.  Errors: -1 opts, -2 m, -3 n, -4 A, -5 lda, -6 b (+p),
+ * -7 q, -9 U/ldu, -11 D, -12 V/ldv. */
+RANDUTV_API int randutv_rsvd(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
+                             int32_t q, uint64_t seed, double* U, int64_t ldu, double* D, double* V, int64_t ldv);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU.  A and T are distributed in 1-D
  * block-cyclic column blocks of width b: global column block j (columns

@@ -78,6 +78,9 @@ def lib():
     L.randutv_strerror.restype = ctypes.c_char_p
     L.randutv_version.restype = ctypes.c_char_p
     L.randutv_gaussian.argtypes = [c_vp, c_i64, c_i64, c_i64, c_u64, c_u32, c_u32, c_vp]
+    L.randutv_rsvd.argtypes = [ctypes.POINTER(_Opts), c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_u64, c_vp, c_i64,
+                               c_vp, c_vp, c_i64]
+    L.randutv_rsvd.restype = ctypes.c_int
     L.randutv_dgemm.argtypes = [c_i32, c_i32, c_i64, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp, c_i64, c_dbl, c_vp,
                                 c_i64, c_vp]
     L.randutv_panel_qr.argtypes = [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]
@@ -106,7 +109,7 @@ EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "ra
             "randutv_profile_end", "randutv_profile_class_name", "randutv_profile_timeline", "randutv_nccl_unique_id",
             "randutv_comm_init_nccl", "randutv_comm_init_loopback", "randutv_comm_destroy",
             "randutv_comm_local_ranks", "randutv_dist_local_cols", "randutv_dist_global_col",
-            "randutv_factor_dist"]
+            "randutv_factor_dist", "randutv_rsvd"]
 
 
 def launch_count() -> int:
@@ -246,6 +249,22 @@ def _randutv_host(A: np.ndarray, b, q, seed, k_stop, tol, reortho, with_uv, qr_m
 def factor_raw(m, n, A_ptr, lda, b, q, seed, k_stop, U_ptr, T_ptr, V_ptr) -> int:
     """Direct randutv_factor call on raw pointers (host or device)."""
     return lib().randutv_factor(m, n, A_ptr, lda, b, q, seed, k_stop, U_ptr, T_ptr, V_ptr)
+
+
+def rsvd(A, b: int, q: int, seed: int, oversample: int = 0, reortho: bool = True, qr_mode: int = 0, stream=None):
+    """Randomized SVD (Remark remark:RSVD): A ~ U diag(D) V^T, rank b.  Returns (U, D, V)."""
+    torch = _torch()
+    A = as_colmajor(A)
+    m, n = A.shape
+    U = empty_cm(m, b, A.device)
+    V = empty_cm(n, b, A.device)
+    D = torch.empty(b, dtype=torch.float64, device=A.device)
+    opts = _Opts(stream=_stream(stream, A.device).value, no_reortho=0 if reortho else 1, qr_mode=int(qr_mode),
+                 oversample=int(oversample))
+    _check(lib().randutv_rsvd(ctypes.byref(opts), m, n, A.data_ptr(), _ld(A), int(b), int(q),
+                              int(seed) & (2**64 - 1), U.data_ptr(), _ld(U), D.data_ptr(), V.data_ptr(), _ld(V)),
+           "randutv_rsvd")
+    return U, D, V
 
 
 def workspace_size(m, n, b, q, with_uv=True) -> int:

@@ -820,6 +820,105 @@ int randutv_panel_qr(int64_t m, int64_t b, double* V, int64_t ldv, double* R, in
   return randutv_panel_qr_ex(m, b, V, ldv, R, ldr, tau, Tw, ldt, 0, nullptr, stream);
 }
 
+// Randomized SVD (Remark remark:RSVD): the first stage is the
+// sketch of one randUTV step (Philox G of step 0, power loop with
+// re-orthonormalization, Householder-equivalent QR for Q), the second stage
+// B = A Q, B = Q_B R_B, R_B = Us D Vs^T, U = Q_B Us, V = Q Vs.
+int randutv_rsvd(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q,
+                 uint64_t seed, double* U, int64_t ldu, double* D, double* V, int64_t ldv) {
+  randutv_opts o{};
+  if (opts) o = *opts;
+  if (o.oversample < 0 || o.qr_mode < 0 || o.qr_mode > 1) return -1;
+  if (m < 1) return -2;
+  if (n < 1) return -3;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  const int64_t bs = b + o.oversample;
+  if (b < 1 || bs > std::min(m, n) || bs > RANDUTV_MAX_B) return -6;
+  if (q < 0) return -7;
+  if (!U || ldu < m) return -9;
+  if (!D) return -11;
+  if (!V || ldv < n) return -12;
+  std::lock_guard<std::mutex> lock(g_mu);
+  try {
+    cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+    const int64_t mx = std::max(m, n);
+    Arena ar;
+    ar.dry = true;
+    auto carve_rsvd = [&](Arena& a, double** bufs, QrWork& qw) {
+      bufs[0] = a.take<double>(size_t(m) * bs);   // G, then B = A Q
+      bufs[1] = a.take<double>(size_t(n) * bs);   // Y
+      bufs[2] = a.take<double>(size_t(n) * bs);   // Y2 / Q
+      bufs[3] = a.take<double>(size_t(m) * bs);   // Z, then Q_B
+      bufs[4] = a.take<double>(size_t(bs) * bs);  // R (of Y, then of B)
+      bufs[5] = a.take<double>(size_t(bs) * bs);  // T_w
+      bufs[6] = a.take<double>(size_t(bs) * bs);  // tmp
+      bufs[7] = a.take<double>(size_t(bs));       // tau
+      bufs[8] = a.take<double>(size_t(bs));       // D (all bs)
+      bufs[9] = a.take<double>(size_t(bs) * bs);  // Us
+      bufs[10] = a.take<double>(size_t(bs) * bs); // Vs
+      bufs[11] = a.take<double>(jacobi_work_elems(1, (int)bs));
+      qw.part_elems = size_t(8) * mx * bs + size_t(148) * 32 * 1024;
+      qw.part = a.take<double>(qw.part_elems);
+      qw.sfull = a.take<double>(size_t(32) * bs);
+      qw.s2 = a.take<double>(size_t(32) * bs);
+      qw.z = a.take<double>(size_t(32) * bs);
+      qw.q1_elems = size_t(mx) * bs;
+      qw.q1 = a.take<double>(qw.q1_elems);
+      qw.small = a.take<double>(small_work_elems(bs));
+    };
+    double* bf[12];
+    QrWork qw{};
+    carve_rsvd(ar, bf, qw);
+    void* ws = cached_ws(ar.off + 4096);
+    if (!ws) return RANDUTV_ERR_NOMEM;
+    Arena ar2;
+    ar2.base = (char*)ws;
+    ar2.size = ar.off + 4096;
+    carve_rsvd(ar2, bf, qw);
+    qw.mode = o.qr_mode;
+    double *G = bf[0], *Y = bf[1], *Y2 = bf[2], *Z = bf[3], *R = bf[4], *Tw = bf[5], *tmp = bf[6], *tau = bf[7],
+           *Dall = bf[8], *Us = bf[9], *Vs = bf[10], *jw = bf[11];
+    auto dgq = [&](bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* X, int64_t ldx, const double* Bm,
+                   int64_t ldb, double* C, int64_t ldc) {
+      dgemm(st, ta, tb, M, N, K, 1.0, X, ldx, Bm, ldb, 0.0, C, ldc, qw.part, qw.part_elems);
+    };
+    set_gemm_role(C_GEMM_SKETCH);
+    gaussian_fill(st, G, m, m, bs, seed, 0u, 0u);                       // step 1
+    dgq(true, false, n, bs, m, A, lda, G, m, Y, n);                     // Y = A^T G
+    for (int it = 0; it < q; ++it) {                                    // step 2
+      if (o.no_reortho == 0) {
+        int rc = rutv::reortho(st, n, bs, Y, n, Y2, n, tmp, Tw, tau, qw);
+        if (rc != OK) return rc;
+        std::swap(Y, Y2);
+      }
+      dgq(false, false, m, bs, n, A, lda, Y, n, Z, m);                  // Z = A Y
+      dgq(true, false, n, bs, m, A, lda, Z, m, Y, n);                   // Y = A^T Z
+    }
+    set_gemm_role(C_GEMM_QR);
+    int rc = panel_qr(st, n, bs, Y, n, R, bs, tau, Tw, bs, qw);         // step 3: Q = orth(Y)
+    if (rc != OK) return rc;
+    thin_q(st, n, bs, Y, n, Tw, bs, Y2, n, tmp, qw.part, qw.part_elems);
+    set_gemm_role(C_GEMM_OTHER);
+    dgq(false, false, m, bs, n, A, lda, Y2, n, G, m);                   // B = A Q
+    set_gemm_role(C_GEMM_QR);
+    rc = panel_qr(st, m, bs, G, m, R, bs, tau, Tw, bs, qw);             // B = Q_B R_B
+    if (rc != OK) return rc;
+    thin_q(st, m, bs, G, m, Tw, bs, Z, m, tmp, qw.part, qw.part_elems);
+    jacobi_svd_batched(st, 1, (int)bs, R, bs, bs * bs, Dall, Us, Vs, jw, nullptr);  // R_B = Us D Vs^T
+    set_gemm_role(C_GEMM_OTHER);
+    dgq(false, false, m, b, bs, Z, m, Us, bs, U, ldu);                  // U = Q_B Us(:, 1:b)
+    dgq(false, false, n, b, bs, Y2, n, Vs, bs, V, ldv);                 // V = Q Vs(:, 1:b)
+    RUTV_CK(cudaMemcpyAsync(D, Dall, sizeof(double) * b, cudaMemcpyDeviceToDevice, st));
+    return RANDUTV_OK;
+  } catch (const CudaError& e) {
+    fprintf(stderr, "randutv_rsvd: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);
+    return e.e == cudaErrorMemoryAllocation ? RANDUTV_ERR_NOMEM : RANDUTV_ERR_CUDA;
+  } catch (int code) {
+    return code;
+  }
+}
+
 int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t ldr, int64_t strideR, double* D,
                               double* Us, double* Vs, int32_t* sweeps, void* stream) {
   if (batch < 0) return -1;

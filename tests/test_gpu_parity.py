@@ -304,3 +304,28 @@ def test_randutv_fat_parity(m, n, b, q, uv):
     if uv:
         inv = invariants(A, to_host(U), Th, to_host(V))
         assert inv["recon"] <= 1e-13 * n and inv["orth_u"] <= 1e-13 * n and inv["orth_v"] <= 1e-13 * n
+
+
+# ----------------------------------------------------------------------------- randomized SVD (NEXT row 3)
+@pytest.mark.parametrize("m,n,b,q,p,decay", [(500, 400, 50, 1, 0, 0.99), (1000, 800, 64, 2, 10, 0.97),
+                                             (3000, 2000, 128, 1, 5, 0.995), (600, 700, 96, 0, 0, 0.98)])
+def test_rsvd_vs_oracle(m, n, b, q, p, decay):
+    """randutv_rsvd (Remark remark:RSVD) vs the oracle on the same Philox G:
+    D within the parity rule, the approximation error ||A - U D V^T||_F within
+    1e-8 relative, U and V orthonormal."""
+    rng = np.random.default_rng(m + n)
+    k = min(m, n)
+    s = decay ** np.arange(k)
+    A = (np.linalg.qr(rng.standard_normal((m, k)))[0] * s) @ np.linalg.qr(rng.standard_normal((n, k)))[0].T
+    Uo, Do, Vo, _ = oracle.rsvd(A, b, q, seed=11, p=p)
+    U, D, V = P.rsvd(to_dev(A), b, q, 11, oversample=p)
+    torch.cuda.synchronize()
+    U, D, V = to_host(U), to_host(D), to_host(V)
+    a = np.linalg.norm(A)
+    floor = max(m, n) * EPS * a
+    assert np.all(np.abs(D - Do) <= 1e-10 * Do + floor)
+    e_gpu = np.linalg.norm(A - (U * D) @ V.T)
+    e_orc = np.linalg.norm(A - (Uo * Do) @ Vo.T)
+    assert abs(e_gpu - e_orc) <= 1e-8 * e_orc + floor
+    assert np.linalg.norm(U.T @ U - np.eye(b)) < 1e-13 * m and np.linalg.norm(V.T @ V - np.eye(b)) < 1e-13 * n
+    assert np.all(np.diff(D) <= 0)
