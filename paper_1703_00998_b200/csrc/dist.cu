@@ -217,6 +217,8 @@ struct RankWork {
   double *piece, *gath, *Yfull, *scal, *nrm;
   int* flag;
   int* sweeps;
+  int* qflags;  // optimistic CholeskyQR decision flags (device)
+  int qflags_cap;
   size_t part_elems;
   QrWork qw;
 };
@@ -265,6 +267,8 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.nrm = ar.take<double>(8192);
   w.flag = ar.take<int>(16);
   w.sweeps = ar.take<int>(size_t(sb) + 16);
+  w.qflags_cap = int(16 * sb + 16);  // reortho + QR(Y) + panel-QR decisions
+  w.qflags = ar.take<int>(size_t(w.qflags_cap));
   w.qw.part = w.part;
   w.qw.part_elems = w.part_elems;
   w.qw.sfull = ar.take<double>(size_t(32) * b);
@@ -330,7 +334,10 @@ class DistFactor {
     st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
   }
 
-  int run(randutv_info* info);
+  // optimistic: CholeskyQR decisions go to device flags instead of host
+  // synchronisations; returns kDistRetry if any rank raised one (all ranks see
+  // the allreduced verdict and retry together in the synchronous mode).
+  int run(randutv_info* info, bool optimistic);
 
  private:
   Comm& comm;
@@ -344,6 +351,12 @@ class DistFactor {
   cudaStream_t st;
   int fallbacks = 0;
   double a_fro_ = 0.0;
+  bool opt_ = false;
+  std::vector<int> nflags_;  // per local rank: optimistic flag slots used
+  int* next_flag(size_t l) {
+    auto& w = L[l].w;
+    return (nflags_[l] < w.qflags_cap) ? w.qflags + nflags_[l]++ : nullptr;
+  }
   std::vector<double*> bufs(double* RankWork::*member) {
     std::vector<double*> v;
     for (auto& lr : L) v.push_back(lr.w.*member);
@@ -412,10 +425,29 @@ class DistFactor {
   }
 };
 
-int DistFactor::run(randutv_info* info) {
+constexpr int kDistRetry = 1000;
+
+// low-priority side stream of this device for the deferred SVD chunks
+cudaStream_t dist_side_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, least));
+  }
+  return streams[dev];
+}
+
+int DistFactor::run(randutv_info* info, bool optimistic) {
   const bool reortho = (o.no_reortho == 0);
   const int64_t s = std::min(cdiv(m, b), cdiv(n, b));
   const int bp = small_pad(b);
+  opt_ = optimistic && o.qr_mode == 0;
+  nflags_.assign(L.size(), 0);
+  fallbacks = 0;
 
   // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
   for (auto& lr : L) {
@@ -427,25 +459,70 @@ int DistFactor::run(randutv_info* info) {
     }
   }
   {
-    // pack [sum of squares, non-finite flag] and allreduce
+    // pack [sum of squares, non-finite flag, T aliases A] and allreduce
     for (auto& lr : L) {
       RUTV_CK(cudaMemcpyAsync(lr.w.pack, lr.w.scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
       int hf = read_int_sync(st, lr.w.flag);
-      double fv = hf ? 1.0 : 0.0;
-      RUTV_CK(cudaMemcpyAsync(lr.w.pack + 1, &fv, sizeof(double), cudaMemcpyHostToDevice, st));
+      double fv[2] = {hf ? 1.0 : 0.0, 0.0};
+      if (lr.nl > 0) {  // an in-place factorization cannot be redone from A
+        const char* a0 = (const char*)lr.A;
+        const char* a1 = a0 + sizeof(double) * (size_t(lr.lda) * (lr.nl - 1) + m);
+        const char* t0 = (const char*)lr.T;
+        const char* t1 = t0 + sizeof(double) * (size_t(lr.ldt) * (lr.nl - 1) + m);
+        fv[1] = (t0 < a1 && a0 < t1) ? 1.0 : 0.0;
+      }
+      RUTV_CK(cudaMemcpyAsync(lr.w.pack + 1, fv, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+      RUTV_CK(cudaStreamSynchronize(st));
     }
-    comm.allreduce(bufs(&RankWork::pack), 2, st);
-    double h[2];
-    RUTV_CK(cudaMemcpyAsync(h, L[0].w.pack, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    comm.allreduce(bufs(&RankWork::pack), 3, st);
+    double h[3];
+    RUTV_CK(cudaMemcpyAsync(h, L[0].w.pack, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     RUTV_CK(cudaStreamSynchronize(st));
     if (h[1] != 0.0) return RANDUTV_ERR_NONFINITE;
     a_fro_ = std::sqrt(h[0]);
+    if (h[2] != 0.0) opt_ = false;
   }
 
   int64_t steps = 0, k_done = 0;
   bool final_block = false;
   int64_t r0f = 0, mif = 0, nif = 0, pf = 0;
   std::vector<int64_t> nt(L.size()), c0(L.size());
+
+  // Deferred b x b SVDs (R11 is on every rank) in chunks of 8 steps on a
+  // low-priority side stream, as in the single-GPU driver (R13).
+  constexpr int64_t kSvdChunk = 8;
+  const bool svd_side = jacobi_single_launch((int)b);
+  cudaStream_t side = svd_side ? dist_side_stream() : nullptr;
+  struct SvdChunk {
+    int64_t s0, s1;
+    cudaEvent_t done;
+  };
+  std::vector<SvdChunk> chunks;
+  std::vector<cudaEvent_t> evs;
+  int64_t svd_done = 0;
+  auto launch_svd_chunk = [&]() {
+    if (steps <= svd_done) return;
+    cudaEvent_t fork, done;
+    RUTV_CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    evs.push_back(fork);
+    evs.push_back(done);
+    RUTV_CK(cudaEventRecord(fork, st));
+    RUTV_CK(cudaStreamWaitEvent(side, fork, 0));
+    const int64_t s0 = svd_done, cnt = steps - svd_done;
+    for (auto& lr : L)
+      jacobi_svd_batched(side, (int)cnt, (int)b, lr.w.Rall + size_t(s0) * b * b, b, b * b, lr.w.Dall + s0 * b,
+                         lr.w.Usall + size_t(s0) * b * b, lr.w.Vsall + size_t(s0) * b * b,
+                         lr.w.jwork + jacobi_work_elems((int)s0, (int)b), lr.w.sweeps + s0);
+    RUTV_CK(cudaEventRecord(done, side));
+    chunks.push_back({s0, steps, done});
+    svd_done = steps;
+  };
+  auto drop_events = [&]() {
+    if (side) RUTV_CK(cudaStreamSynchronize(side));
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    evs.clear();
+  };
 
   for (int64_t i = 1; i <= s; ++i) {
     const int64_t p = i - 1, r0 = b * p;
@@ -470,10 +547,19 @@ int DistFactor::run(randutv_info* info) {
         if (reortho) {
           set_gemm_role(C_GEMM_QR);
           dist_gram_chol(&RankWork::Y, nt, 1);
-          double h[3];
-          RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-          RUTV_CK(cudaStreamSynchronize(st));
-          const bool ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
+          bool ok;
+          if (opt_) {  // decision flags on the device, checked once after the loop
+            for (size_t l = 0; l < L.size(); ++l) {
+              int* f = next_flag(l);
+              if (f) reortho_flag(st, L[l].sw.stats, 1e4, f);
+            }
+            ok = true;
+          } else {
+            double h[3];
+            RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            RUTV_CK(cudaStreamSynchronize(st));
+            ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
+          }
           if (ok) {
             for (size_t l = 0; l < L.size(); ++l) {
               auto& lr = L[l];
@@ -518,8 +604,14 @@ int DistFactor::run(randutv_info* info) {
           if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, std::max<int64_t>(nt[l], 1), lr.w.pack, b);
         }
         comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
-        for (auto& lr : L) small_recon(st, b, lr.sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b);
-        qr_ok = read_int_sync(st, L[0].sw.flag) == 0;
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          SmallWork sw = lr.sw;
+          int* f = opt_ ? next_flag(l) : nullptr;
+          if (f) sw.flag = f;
+          small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b);
+        }
+        qr_ok = opt_ ? true : (read_int_sync(st, L[0].sw.flag) == 0);
         if (qr_ok) {
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
@@ -559,6 +651,11 @@ int DistFactor::run(randutv_info* info) {
         QrWork qw = lr.w.qw;
         qw.mode = o.qr_mode;
         qw.fallbacks = &fallbacks;
+        if (opt_) {
+          qw.dev_flags = lr.w.qflags;
+          qw.flag_count = &nflags_[l];
+          qw.flag_cap = lr.w.qflags_cap;
+        }
         int rc = panel_qr(st, mi, b, Wu, mi, Wu + wun + size_t(b) * b, b, lr.w.tau, Wu + wun, b, qw);
         if (rc != OK) return rc;
         // T(I2,J2) = R11 (replaced by D after the SVD), T(I3,J2) = 0
@@ -582,6 +679,7 @@ int DistFactor::run(randutv_info* info) {
       }
       ++steps;
       k_done = std::min(b * i, n);
+      if (svd_side && steps - svd_done >= kSvdChunk) launch_svd_chunk();
       if (o.tol > 0.0) {  // ||T(I3, J3)||_F over all ranks
         const int64_t e2 = std::min(b * i, m);
         for (size_t l = 0; l < L.size(); ++l) {
@@ -623,14 +721,44 @@ int DistFactor::run(randutv_info* info) {
     }
   }
 
-  // ---- b x b SVDs (R11 on every rank: run redundantly; P:964) and folds (P:965-968)
+  // ---- optimistic CholeskyQR decisions: one check for the whole loop, the
+  // verdict allreduced so that every rank retries (or not) together
+  if (opt_) {
+    for (size_t l = 0; l < L.size(); ++l) {
+      double any = 0.0;
+      if (nflags_[l] > 0) {
+        std::vector<int> hf(nflags_[l]);
+        RUTV_CK(cudaMemcpyAsync(hf.data(), L[l].w.qflags, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, st));
+        RUTV_CK(cudaStreamSynchronize(st));
+        for (int f : hf) any += f ? 1.0 : 0.0;
+      }
+      RUTV_CK(cudaMemcpyAsync(L[l].w.pack, &any, sizeof(double), cudaMemcpyHostToDevice, st));
+      RUTV_CK(cudaStreamSynchronize(st));
+    }
+    comm.allreduce(bufs(&RankWork::pack), 1, st);
+    double tot = 0.0;
+    RUTV_CK(cudaMemcpyAsync(&tot, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RUTV_CK(cudaStreamSynchronize(st));
+    if (tot != 0.0) {
+      drop_events();
+      return kDistRetry;
+    }
+  }
+
+  // ---- b x b SVDs (R11 on every rank: run redundantly; P:964) and folds
+  // (P:965-968), chunk by chunk as the side-stream SVDs complete
   set_gemm_role(C_GEMM_OTHER);
-  for (auto& lr : L) {
-    if (steps > 0)
+  if (svd_side) {
+    launch_svd_chunk();
+  } else if (steps > 0) {
+    for (auto& lr : L)
       jacobi_svd_batched(st, (int)steps, (int)b, lr.w.Rall, b, b * b, lr.w.Dall, lr.w.Usall, lr.w.Vsall, lr.w.jwork,
                          lr.w.sweeps);
+    chunks.push_back({0, steps, nullptr});
   }
-  for (int64_t si = 0; si < steps; ++si) {
+  for (const SvdChunk& ch : chunks) {
+  if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
+  for (int64_t si = ch.s0; si < ch.s1; ++si) {
     const int64_t r0 = b * si;
     const int owner = int(si % P);
     for (size_t l = 0; l < L.size(); ++l) {
@@ -652,6 +780,9 @@ int DistFactor::run(randutv_info* info) {
       }
     }
   }
+  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  evs.clear();
   if (final_block) {
     const int owner = int(pf % P);
     for (auto& lr : L) {
@@ -838,8 +969,12 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
       lr.w.qw.mode = o.qr_mode;
       lr.sw = rutv::carve_small(lr.w.small, b);
     }
+    // optimistic first (no per-panel host synchronisation; run() falls back to
+    // the synchronous mode on every rank if any rank factors in place)
     rutv::DistFactor f(c, o, m, n, b, q, seed, k_stop, L);
-    return f.run(info);
+    int rc = f.run(info, true);
+    if (rc == rutv::kDistRetry) rc = f.run(info, false);
+    return rc;
   } catch (const rutv::CudaError& e) {
     fprintf(stderr, "randutv_factor_dist: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);
     return RANDUTV_ERR_CUDA;
