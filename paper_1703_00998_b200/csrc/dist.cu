@@ -338,6 +338,10 @@ class DistFactor {
   // synchronisations; returns kDistRetry if any rank raised one (all ranks see
   // the allreduced verdict and retry together in the synchronous mode).
   int run(randutv_info* info, bool optimistic);
+  ~DistFactor() {
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+  }
 
  private:
   Comm& comm;
@@ -352,6 +356,7 @@ class DistFactor {
   int fallbacks = 0;
   double a_fro_ = 0.0;
   bool opt_ = false;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;  // owner's right-apply overlap
   std::vector<int> nflags_;  // per local rank: optimistic flag slots used
   int* next_flag(size_t l) {
     auto& w = L[l].w;
@@ -441,6 +446,20 @@ cudaStream_t dist_side_stream() {
   return streams[dev];
 }
 
+// low-priority side stream for the owner's trailing right-apply update
+cudaStream_t dist_update_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, least));
+  }
+  return streams[dev];
+}
+
 int DistFactor::run(randutv_info* info, bool optimistic) {
   const bool reortho = (o.no_reortho == 0);
   const int64_t s = std::min(cdiv(m, b), cdiv(n, b));
@@ -448,6 +467,8 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   opt_ = optimistic && o.qr_mode == 0;
   nflags_.assign(L.size(), 0);
   fallbacks = 0;
+  if (!ev_fork_) RUTV_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  if (!ev_join_) RUTV_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
 
   // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
   for (auto& lr : L) {
@@ -634,11 +655,30 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
            std::max<int64_t>(nt[l], 1), 0.0, lr.w.P, m);
       }
       comm.allreduce(bufs(&RankWork::P), size_t(m) * b, st);
+      bool joined = false;
       for (size_t l = 0; l < L.size(); ++l) {
         auto& lr = L[l];
+        const int64_t ldy = std::max<int64_t>(nt[l], 1);
         dg(lr.w, st, false, false, m, b, b, 1.0, lr.w.P, m, Tv[l], b, 0.0, lr.w.P2, m);
-        dg(lr.w, st, false, true, m, nt[l], b, -1.0, lr.w.P2, m, lr.w.Y, std::max<int64_t>(nt[l], 1), 1.0,
-           lr.T + c0[l] * lr.ldt, lr.ldt);
+        if (lr.r != owner) {
+          dg(lr.w, st, false, true, m, nt[l], b, -1.0, lr.w.P2, m, lr.w.Y, ldy, 1.0, lr.T + c0[l] * lr.ldt, lr.ldt);
+          continue;
+        }
+        // owner: the panel QR below reads only T(r0:m, block p) -- update it
+        // first; the rest of its rank-b update runs on a low-priority side
+        // stream concurrently with the panel QR (the other ranks wait for the
+        // owner's broadcast), joined before the left apply.  Unsplit GEMMs.
+        double* TJ = lr.T + c0[l] * lr.ldt;
+        dg(lr.w, st, false, true, mi, b, b, -1.0, lr.w.P2 + r0, m, lr.w.Y, ldy, 1.0, TJ + r0, lr.ldt);
+        cudaStream_t upd = dist_update_stream();
+        RUTV_CK(cudaEventRecord(ev_fork_, st));
+        RUTV_CK(cudaStreamWaitEvent(upd, ev_fork_, 0));
+        if (r0 > 0) dgemm(upd, false, true, r0, b, b, -1.0, lr.w.P2, m, lr.w.Y, ldy, 1.0, TJ, lr.ldt, nullptr, 0);
+        if (nt[l] > b)
+          dgemm(upd, false, true, m, nt[l] - b, b, -1.0, lr.w.P2, m, lr.w.Y + b, ldy, 1.0, TJ + b * lr.ldt, lr.ldt,
+                nullptr, 0);
+        RUTV_CK(cudaEventRecord(ev_join_, upd));
+        joined = true;
       }
       // ---- panel QR on the owner of block p, broadcast (W_u, T_u, R11)
       const size_t wun = size_t(mi) * b;
@@ -666,6 +706,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       for (auto& lr : L)  // keep R11 for the deferred SVD
         copy_matrix(st, b, b, lr.w.pack + wun + size_t(b) * b, b, lr.w.Rall + size_t(si) * b * b, b);
       // ---- left apply to the local columns right of block p
+      if (joined) RUTV_CK(cudaStreamWaitEvent(st, ev_join_, 0));
       set_gemm_role(C_GEMM_LEFT);
       for (size_t l = 0; l < L.size(); ++l) {
         auto& lr = L[l];
