@@ -358,6 +358,8 @@ class DistFactor {
   bool opt_ = false;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;  // owner's right-apply overlap
   std::vector<int> nflags_;  // per local rank: optimistic flag slots used
+  // number of steps si < s with si = r (mod P), i.e. the slot of the next owned step
+  int64_t own_slot(int64_t s, int r) const { return blocks_before(s, r, P); }
   int* next_flag(size_t l) {
     auto& w = L[l].w;
     return (nflags_[l] < w.qflags_cap) ? w.qflags + nflags_[l]++ : nullptr;
@@ -530,11 +532,15 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     evs.push_back(done);
     RUTV_CK(cudaEventRecord(fork, st));
     RUTV_CK(cudaStreamWaitEvent(side, fork, 0));
-    const int64_t s0 = svd_done, cnt = steps - svd_done;
-    for (auto& lr : L)
-      jacobi_svd_batched(side, (int)cnt, (int)b, lr.w.Rall + size_t(s0) * b * b, b, b * b, lr.w.Dall + s0 * b,
-                         lr.w.Usall + size_t(s0) * b * b, lr.w.Vsall + size_t(s0) * b * b,
-                         lr.w.jwork + jacobi_work_elems((int)s0, (int)b), lr.w.sweeps + s0);
+    const int64_t s0 = svd_done, s1 = steps;
+    for (auto& lr : L) {  // this rank's own blocks only: steps si = r (mod P), slot j = si / P
+      const int64_t j0 = own_slot(s0, lr.r), j1 = own_slot(s1, lr.r);
+      if (j1 > j0)
+        jacobi_svd_batched(side, (int)(j1 - j0), (int)b, lr.w.Rall + size_t(j0 * P + lr.r) * b * b, b,
+                           int64_t(P) * b * b, lr.w.Dall + j0 * b, lr.w.Usall + size_t(j0) * b * b,
+                           lr.w.Vsall + size_t(j0) * b * b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b),
+                           lr.w.sweeps + j0);
+    }
     RUTV_CK(cudaEventRecord(done, side));
     chunks.push_back({s0, steps, done});
     svd_done = steps;
@@ -792,9 +798,12 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   if (svd_side) {
     launch_svd_chunk();
   } else if (steps > 0) {
-    for (auto& lr : L)
-      jacobi_svd_batched(st, (int)steps, (int)b, lr.w.Rall, b, b * b, lr.w.Dall, lr.w.Usall, lr.w.Vsall, lr.w.jwork,
-                         lr.w.sweeps);
+    for (auto& lr : L) {
+      const int64_t j1 = own_slot(steps, lr.r);
+      if (j1 > 0)
+        jacobi_svd_batched(st, (int)j1, (int)b, lr.w.Rall + size_t(lr.r) * b * b, b, int64_t(P) * b * b, lr.w.Dall,
+                           lr.w.Usall, lr.w.Vsall, lr.w.jwork, lr.w.sweeps);
+    }
     chunks.push_back({0, steps, nullptr});
   }
   for (const SvdChunk& ch : chunks) {
@@ -802,10 +811,15 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   for (int64_t si = ch.s0; si < ch.s1; ++si) {
     const int64_t r0 = b * si;
     const int owner = int(si % P);
+    const int64_t js = si / P;  // the owner's slot of step si
+    // Us of step si (computed by its owner) -> every rank, for the row fold
+    for (auto& lr : L)
+      if (lr.r == owner) copy_matrix(st, b, b, lr.w.Usall + size_t(js) * b * b, b, lr.w.pack, b);
+    comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
     for (size_t l = 0; l < L.size(); ++l) {
       auto& lr = L[l];
-      const double* Us = lr.w.Usall + size_t(si) * b * b;
-      const double* Vs = lr.w.Vsall + size_t(si) * b * b;
+      const double* Us = lr.w.pack;
+      const double* Vs = lr.w.Vsall + size_t(js) * b * b;  // used on the owner only
       const int64_t cb = b * blocks_before(si, lr.r, P);  // local offset of block si (if owned) / of J3
       const int64_t cs = cb + ((lr.r == owner) ? b : 0), nc = lr.nl - cs;
       if (nc > 0) {  // T(I2, J3) = Us^T T(I2, J3) on the local columns
@@ -813,7 +827,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         copy_matrix(st, b, nc, lr.w.fold, b, lr.T + r0 + cs * lr.ldt, lr.ldt);
       }
       if (lr.r == owner) {
-        write_diag_block(st, b, b, lr.w.Dall + si * b, lr.T + r0 + cb * lr.ldt, lr.ldt);
+        write_diag_block(st, b, b, lr.w.Dall + js * b, lr.T + r0 + cb * lr.ldt, lr.ldt);
         if (r0 > 0) {  // T(I1, J2) = T(I1, J2) Vs
           dg(lr.w, st, false, false, r0, b, b, 1.0, lr.T + cb * lr.ldt, lr.ldt, Vs, b, 0.0, lr.w.fold, r0);
           copy_matrix(st, r0, b, lr.w.fold, r0, lr.T + cb * lr.ldt, lr.ldt);
