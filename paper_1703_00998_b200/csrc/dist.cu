@@ -315,8 +315,9 @@ struct LocalRank {
 };
 
 void dg(const RankWork& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
-        const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
-  dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems);
+        const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+        bool b_upper = false) {
+  dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems, 0, b_upper);
 }
 
 int read_int_sync(cudaStream_t st, const int* d) {
@@ -591,7 +592,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
             for (size_t l = 0; l < L.size(); ++l) {
               auto& lr = L[l];
               dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
-                 lr.w.Y2, std::max<int64_t>(nt[l], 1));
+                 lr.w.Y2, std::max<int64_t>(nt[l], 1), true);
             }
           } else {
             int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr);
@@ -622,7 +623,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         for (size_t l = 0; l < L.size(); ++l) {
           auto& lr = L[l];
           dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
-             lr.w.q1, std::max<int64_t>(nt[l], 1));
+             lr.w.q1, std::max<int64_t>(nt[l], 1), true);
         }
         dist_gram_chol(&RankWork::q1, nt, 2);
         // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
@@ -643,7 +644,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
             if (nt[l] > 0)
-              dg(lr.w, st, false, false, nt[l], b, b, -1.0, lr.w.q1, nt[l], lr.sw.M, bp, 0.0, lr.w.Y, nt[l]);
+              dg(lr.w, st, false, false, nt[l], b, b, -1.0, lr.w.q1, nt[l], lr.sw.M, bp, 0.0, lr.w.Y, nt[l], true);
             if (lr.r == owner) small_put_unit_lower(st, b, lr.sw, lr.w.Y, std::max<int64_t>(nt[l], 1));
           }
         }

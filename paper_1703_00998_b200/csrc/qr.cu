@@ -508,14 +508,15 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     const int bp = sw.bp;
     dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems);        // G1
     small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
-    dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems);     // Q1
+    dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems, 0, true);  // Q1
     dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems);      // G2
     const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
     small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt);
     if (optimistic || read_flag_sync(st, sw.flag) == 0) {
       if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
-        dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems);
+        dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems, 0,
+              true);
       small_put_unit_lower(st, b, sw, V, ldv);
       return OK;
     }
@@ -545,7 +546,7 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
       ok = h[0] == 0.0 && h[2] <= kKappaMax * h[1];
     }
     if (ok) {
-      dgemm(st, false, false, m, b, b, 1.0, Y, ldy, sw.R1i, bp, 0.0, Q, ldq, w.part, w.part_elems);
+      dgemm(st, false, false, m, b, b, 1.0, Y, ldy, sw.R1i, bp, 0.0, Q, ldq, w.part, w.part_elems, 0, true);
       return OK;
     }
     if (w.fallbacks) ++*w.fallbacks;
