@@ -243,7 +243,7 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.pack = ar.take<double>(size_t(m) * b + 2 * size_t(b) * b + 64);
   w.q1 = ar.take<double>(size_t(mx) * b);
   w.small = ar.take<double>(small_work_elems(b));
-  w.part_elems = size_t(8) * mx * b + size_t(148) * 32 * 1024;
+  w.part_elems = size_t(12) * mx * b + size_t(148) * 32 * 1024;
   w.part = ar.take<double>(w.part_elems);
   w.fold = ar.take<double>(size_t(mx) * b);
   w.Rall = ar.take<double>(size_t(sb) * b * b);

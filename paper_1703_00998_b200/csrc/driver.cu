@@ -124,7 +124,7 @@ Work carve(Arena& ar, const Plan& p) {
     w.Wu_all = ar.take<double>(p.elems_u);
   }
   w.fold = ar.take<double>(size_t(mx) * b);
-  w.part_elems = size_t(8) * mx * bs + size_t(148) * 32 * 1024;
+  w.part_elems = size_t(12) * mx * bs + size_t(148) * 32 * 1024;
   w.part = ar.take<double>(w.part_elems);
   w.qw.part = w.part;
   w.qw.part_elems = w.part_elems;
@@ -772,7 +772,7 @@ int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t 
   if (ldc < std::max<int64_t>(1, M)) return -13;
   std::lock_guard<std::mutex> lock(g_mu);
   try {
-    size_t part = size_t(8) * std::max<int64_t>(M, 1) * std::max<int64_t>(N, 1) + size_t(148) * 32 * 1024;
+    size_t part = size_t(12) * std::max<int64_t>(M, 1) * std::max<int64_t>(N, 1) + size_t(148) * 32 * 1024;
     part = std::min(part, size_t(1) << 30);
     double* ws = (double*)cached_ws(part * sizeof(double));
     if (!ws) return RANDUTV_ERR_NOMEM;
@@ -795,7 +795,7 @@ int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R,
   if (mode < 0 || mode > 1) return -10;
   std::lock_guard<std::mutex> lock(g_mu);
   try {
-    size_t part = size_t(8) * m * b + size_t(148) * 32 * 1024;
+    size_t part = size_t(12) * m * b + size_t(148) * 32 * 1024;
     size_t extra = size_t(3) * 32 * b + 1024;
     size_t q1 = size_t(m) * b, sm = small_work_elems(b) + 64;
     double* ws = (double*)cached_ws((part + extra + q1 + sm) * sizeof(double));
@@ -858,7 +858,7 @@ int randutv_rsvd(const randutv_opts* opts, int64_t m, int64_t n, const double* A
       bufs[9] = a.take<double>(size_t(bs) * bs);  // Us
       bufs[10] = a.take<double>(size_t(bs) * bs); // Vs
       bufs[11] = a.take<double>(jacobi_work_elems(1, (int)bs));
-      qw.part_elems = size_t(8) * mx * bs + size_t(148) * 32 * 1024;
+      qw.part_elems = size_t(12) * mx * bs + size_t(148) * 32 * 1024;
       qw.part = a.take<double>(qw.part_elems);
       qw.sfull = a.take<double>(size_t(32) * bs);
       qw.s2 = a.take<double>(size_t(32) * bs);
