@@ -215,20 +215,30 @@ RANDUTV_API int randutv_comm_local_ranks(const randutv_comm* comm, int32_t* worl
 RANDUTV_API int64_t randutv_dist_local_cols(int64_t n, int64_t b, int32_t rank, int32_t nranks);
 RANDUTV_API int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_t rank, int32_t nranks);
 
-/* Distributed randutv_factor_ex, T-only mode (U = V = NULL; the paper's "no
- * orthonormal matrices" mode).  A_loc[l], T_loc[l] (device,
- * ld lda_loc[l] / ldt_loc[l] >= m) are the shards of the l-th rank this
- * process drives (randutv_comm_local_ranks order).  T_loc may alias A_loc.
+/* Distributed randutv_factor_ex (PAPER.md:919-989 on 1-D column shards).
+ *  A_loc[l], T_loc[l]  device shards (m x n_loc, ld lda_loc[l] / ldt_loc[l] >= m)
+ *                      of the l-th rank this process drives
+ *                      (randutv_comm_local_ranks order).  T_loc may alias A_loc.
+ *  U_loc[l], V_loc[l]  NULL (both) for the paper's "no orthonormal matrices"
+ *                      mode, else the rank's shards of
+ *                      U (m x randutv_dist_local_cols(m, b, ...), ld ldu >= m)
+ *                      and V (n x n_loc, ld ldv >= n) in the same block-cyclic
+ *                      column layout (U's column block j <-> T's row block j).
+ *                      They are formed by backward accumulation (P:951, 958,
+ *                      967, 969): W_u is broadcast by the panel owner anyway,
+ *                      W_v's row pieces are allgathered once per step at the end.
  * All ranks must pass identical m, n, b, q, seed, k_stop and options.  On
- * return each T_loc holds that rank's columns of T; info is identical on all
- * ranks.  Errors: -1 opts, -2 comm, -3 m, -4 n, -5 A_loc/lda_loc, -7 b, -8 q,
- * -10 k_stop, -11 T_loc/ldt_loc; RANDUTV_ERR_NCCL on a failed collective.
- * Synchronises the stream as randutv_factor_ex does, plus once per step for
- * the (rank-consistent) CholeskyQR fallback decisions. */
+ * return each shard holds that rank's columns of U, T, V; info is identical on
+ * all ranks.  Errors: -1 opts, -2 comm, -3 m, -4 n (n > m unsupported here),
+ * -5 A_loc/lda_loc, -7 b, -8 q, -10 k_stop, -12 U_loc/ldu_loc, -13
+ * T_loc/ldt_loc, -16 V_loc/ldv_loc (or only one of U/V given);
+ * RANDUTV_ERR_UNSUPPORTED for opts->oversample > 0; RANDUTV_ERR_NCCL on a
+ * failed collective.  Synchronises the stream as randutv_factor_ex does. */
 RANDUTV_API int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m, int64_t n,
                                     const double* const* A_loc, const int64_t* lda_loc, int64_t b, int32_t q,
-                                    uint64_t seed, int64_t k_stop, double* const* T_loc, const int64_t* ldt_loc,
-                                    randutv_info* info);
+                                    uint64_t seed, int64_t k_stop, double* const* U_loc, const int64_t* ldu_loc,
+                                    double* const* T_loc, const int64_t* ldt_loc, double* const* V_loc,
+                                    const int64_t* ldv_loc, randutv_info* info);
 
 /* ---------------------------------------------------------------------------
  * Instrumentation (used by bench.py).

@@ -203,6 +203,16 @@ __global__ void scatter_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p
     loc[(k * b + i) + c * ldl] = full[gr + c * ldf];
   }
 }
+// X_loc = the rank-r columns of the rows x rows identity (block-cyclic, width b)
+__global__ void cyclic_identity_k(int64_t rows, int64_t nl, int64_t b, int r, int P, double* __restrict__ X,
+                                  int64_t ldx) {
+  const int64_t tot = rows * nl;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, jl = e / rows;
+    const int64_t g = ((jl / b) * P + r) * b + jl % b;
+    X[i + jl * ldx] = (i == g) ? 1.0 : 0.0;
+  }
+}
 inline int grid_for_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2048)); }
 }  // namespace
 
@@ -215,6 +225,9 @@ struct RankWork {
   double *Rall, *Dall, *Usall, *Vsall, *jwork;
   double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf, *Tfin, *tau, *Ttmp, *Rtmp;
   double *piece, *gath, *Yfull, *scal, *nrm;
+  // U, V formation (DistPlan::uv): replicated W_u / T_u / T_v of every step,
+  // this rank's rows of every W_v
+  double *Wu_all, *Tu_all, *Wvl_all, *Tv_all;
   int* flag;
   int* sweeps;
   int* qflags;  // optimistic CholeskyQR decision flags (device)
@@ -226,7 +239,17 @@ struct RankWork {
 struct DistPlan {
   int64_t m, n, b, s, nrand, nl_max, maxpiece;
   int P;
+  bool uv = false;
+  std::vector<size_t> off_u, off_vl;  // per step: offsets into Wu_all (m_i x b) / Wvl_all (piece_i x b)
+  size_t elems_u = 0, elems_vl = 0;
 };
+
+// rows of W_v of step p held by the rank with the most (padding of the allgather)
+inline int64_t max_piece(int64_t n, int64_t b, int64_t p, int P) {
+  int64_t mp = 1;
+  for (int r = 0; r < P; ++r) mp = std::max(mp, local_cols(n, b, r, P) - b * blocks_before(p, r, P));
+  return mp;
+}
 
 RankWork carve_rank(Arena& ar, const DistPlan& d) {
   RankWork w{};
@@ -265,6 +288,12 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.Yfull = ar.take<double>(size_t(d.n) * b);
   w.scal = ar.take<double>(16);
   w.nrm = ar.take<double>(8192);
+  if (d.uv) {
+    w.Wu_all = ar.take<double>(d.elems_u);
+    w.Tu_all = ar.take<double>(size_t(sb + 1) * b * b);
+    w.Wvl_all = ar.take<double>(d.elems_vl);
+    w.Tv_all = ar.take<double>(size_t(sb) * b * b);
+  }
   w.flag = ar.take<int>(16);
   w.sweeps = ar.take<int>(size_t(sb) + 16);
   w.qflags_cap = int(16 * sb + 16);  // reortho + QR(Y) + panel-QR decisions
@@ -280,8 +309,9 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   return w;
 }
 
-DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P) {
+DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P, bool uv) {
   DistPlan d;
+  d.uv = uv;
   d.m = m;
   d.n = n;
   d.b = b;
@@ -293,6 +323,17 @@ DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P) {
   d.nl_max = 0;
   for (int r = 0; r < P; ++r) d.nl_max = std::max(d.nl_max, local_cols(n, b, r, P));
   d.maxpiece = std::max<int64_t>(d.nl_max, 1);
+  if (uv) {  // randomized steps, then the final (tall) block's reflectors in slot nrand
+    for (int64_t si = 0; si <= d.nrand; ++si) {
+      d.off_u.push_back(d.elems_u);
+      d.elems_u += size_t(m - b * si) * b;
+    }
+    for (int64_t si = 0; si < d.nrand; ++si) {
+      d.off_vl.push_back(d.elems_vl);
+      d.elems_vl += size_t(max_piece(n, b, si, P)) * b;
+    }
+    d.elems_vl = std::max<size_t>(d.elems_vl, 1);
+  }
   return d;
 }
 
@@ -309,6 +350,8 @@ struct LocalRank {
   int64_t lda;
   double* T;
   int64_t ldt;
+  double *U, *V;         // shards of U (m x mloc) and V (n x nl), or NULL (T-only)
+  int64_t ldu, ldv;
   int64_t nl;            // local columns
   RankWork w;
   SmallWork sw;
@@ -330,8 +373,8 @@ int read_int_sync(cudaStream_t st, const int* d) {
 class DistFactor {
  public:
   DistFactor(Comm& c, const randutv_opts& o, int64_t m, int64_t n, int64_t b, int q, uint64_t seed,
-             int64_t k_stop, std::vector<LocalRank>& L)
-      : comm(c), o(o), m(m), n(n), b(b), q(q), seed(seed), k_stop(k_stop), L(L), P(c.P) {
+             int64_t k_stop, std::vector<LocalRank>& L, const DistPlan& plan)
+      : comm(c), o(o), m(m), n(n), b(b), q(q), seed(seed), k_stop(k_stop), L(L), P(c.P), plan_(plan) {
     st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
   }
 
@@ -353,6 +396,7 @@ class DistFactor {
   int64_t k_stop;
   std::vector<LocalRank>& L;
   int P;
+  const DistPlan& plan_;
   cudaStream_t st;
   int fallbacks = 0;
   double a_fro_ = 0.0;
@@ -392,6 +436,12 @@ class DistFactor {
   // Householder fallback for a distributed Y: allgather -> full Y on every rank,
   // panel QR there (redundant), then every rank takes its rows of the result.
   // mode 0: thin Q -> dst (re-orthonormalisation); mode 1: reflectors -> dst, Tv.
+  // U = U_1 ... U_s blockdiag(Us_i), V likewise by
+  // backward accumulation on each rank's column shards: a block reflector
+  // acts on rows, so with W_u replicated (broadcast by the panel owner) the U
+  // update is rank-local; W_v is row-distributed and is allgathered per step.
+  void form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf);
+
   int dist_householder(int64_t p, int64_t ni, double* RankWork::*src, double* RankWork::*dst,
                        const std::vector<int64_t>& nt, int mode, double* const* Tv) {
     int64_t maxpiece = 0;
@@ -654,6 +704,13 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         if (rc != OK) return rc;
         for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
       }
+      if (plan_.uv)  // keep this rank's rows of W_v and T_v for the V formation
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          const int64_t ldy = std::max<int64_t>(nt[l], 1);
+          if (nt[l] > 0) copy_matrix(st, nt[l], b, lr.w.Y, ldy, lr.w.Wvl_all + plan_.off_vl[si], ldy);
+          copy_matrix(st, b, b, Tv[l], b, lr.w.Tv_all + size_t(si) * b * b, b);
+        }
       // ---- right apply to all m rows
       set_gemm_role(C_GEMM_RIGHT);
       for (size_t l = 0; l < L.size(); ++l) {
@@ -710,8 +767,13 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         set_zero(st, mi - b, b, X + b, lr.ldt);
       }
       comm.bcast(bufs(&RankWork::pack), wun + 2 * size_t(b) * b, owner, st);
-      for (auto& lr : L)  // keep R11 for the deferred SVD
+      for (auto& lr : L) {  // keep R11 for the deferred SVD (and W_u, T_u for U)
         copy_matrix(st, b, b, lr.w.pack + wun + size_t(b) * b, b, lr.w.Rall + size_t(si) * b * b, b);
+        if (plan_.uv) {
+          copy_matrix(st, mi, b, lr.w.pack, mi, lr.w.Wu_all + plan_.off_u[si], mi);
+          copy_matrix(st, b, b, lr.w.pack + wun, b, lr.w.Tu_all + size_t(si) * b * b, b);
+        }
+      }
       // ---- left apply to the local columns right of block p
       if (joined) RUTV_CK(cudaStreamWaitEvent(st, ev_join_, 0));
       set_gemm_role(C_GEMM_LEFT);
@@ -762,6 +824,15 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           if (rc != OK) return rc;
         } else {
           copy_matrix(st, ni, ni, X, lr.ldt, lr.w.Rfin, ni);
+        }
+      }
+      if (plan_.uv && mi > ni) {  // the tall block's reflectors to every rank (U formation)
+        for (auto& lr : L)
+          if (lr.r == owner) copy_matrix(st, ni, ni, lr.w.Tfin, ni, lr.w.pack + size_t(mi) * ni, ni);
+        comm.bcast(bufs(&RankWork::pack), size_t(mi) * ni + size_t(ni) * ni, owner, st);
+        for (auto& lr : L) {
+          copy_matrix(st, mi, ni, lr.w.pack, mi, lr.w.Wu_all + plan_.off_u[p], mi);
+          copy_matrix(st, ni, ni, lr.w.pack + size_t(mi) * ni, ni, lr.w.Tu_all + size_t(p) * b * b, ni);
         }
       }
       k_done = n;
@@ -855,6 +926,8 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     }
   }
 
+  if (plan_.uv) form_uv(steps, final_block, r0f, mif, nif, pf);
+
   if (info) {
     info->k_done = k_done;
     info->steps = (int32_t)steps;
@@ -877,6 +950,81 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     RUTV_CK(cudaStreamSynchronize(st));
   }
   return RANDUTV_OK;
+}
+
+void DistFactor::form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf) {
+  set_gemm_role(C_GEMM_OTHER);
+  for (auto& lr : L) {
+    const int64_t mloc = local_cols(m, b, lr.r, P);
+    if (mloc > 0) {
+      ProfScope _p(st, K_MISC, 0.0);
+      count_launch(K_MISC);
+      cyclic_identity_k<<<grid_for_n(m * mloc), 256, 0, st>>>(m, mloc, b, lr.r, P, lr.U, lr.ldu);
+      RUTV_LAUNCH_CK();
+    }
+    if (lr.nl > 0) {
+      ProfScope _p(st, K_MISC, 0.0);
+      count_launch(K_MISC);
+      cyclic_identity_k<<<grid_for_n(n * lr.nl), 256, 0, st>>>(n, lr.nl, b, lr.r, P, lr.V, lr.ldv);
+      RUTV_LAUNCH_CK();
+    }
+  }
+  // X(r0:, local columns of blocks >= p) <- (I - W Tw W^T) X(r0:, ...)   (W rows x k)
+  auto apply_left = [&](LocalRank& lr, double* X, int64_t ldx, int64_t ncols_loc, int64_t p, int64_t rows,
+                        int64_t k, const double* W, int64_t ldw, const double* Tw, int64_t ldtw) {
+    const int64_t cs = b * blocks_before(p, lr.r, P), nc = ncols_loc - cs;
+    if (nc <= 0 || rows <= 0 || k <= 0) return;
+    double* Xb = X + b * p + cs * ldx;
+    dg(lr.w, st, true, false, k, nc, rows, 1.0, W, ldw, Xb, ldx, 0.0, lr.w.fold, k);
+    dg(lr.w, st, false, false, k, nc, k, 1.0, Tw, ldtw, lr.w.fold, k, 0.0, lr.w.P, k);
+    dg(lr.w, st, false, false, rows, nc, k, -1.0, W, ldw, lr.w.P, k, 1.0, Xb, ldx);
+  };
+  if (final_block && mif > nif)
+    for (auto& lr : L)
+      apply_left(lr, lr.U, lr.ldu, local_cols(m, b, lr.r, P), pf, mif, nif, lr.w.Wu_all + plan_.off_u[pf], mif,
+                 lr.w.Tu_all + size_t(pf) * b * b, nif);
+  for (int64_t si = steps - 1; si >= 0; --si) {
+    const int64_t r0 = b * si, mi = m - r0, ni = n - r0;
+    // full W_v of step si on every rank: padded allgather of the row pieces
+    const int64_t mp = max_piece(n, b, si, P);
+    for (auto& lr : L) {
+      const int64_t nt = lr.nl - b * blocks_before(si, lr.r, P), ldy = std::max<int64_t>(nt, 1);
+      set_zero(st, mp, b, lr.w.piece, mp);
+      if (nt > 0) copy_matrix(st, nt, b, lr.w.Wvl_all + plan_.off_vl[si], ldy, lr.w.piece, mp);
+    }
+    comm.allgather(bufs(&RankWork::piece), bufs(&RankWork::gath), size_t(mp) * b, st);
+    for (auto& lr : L) {
+      {
+        ProfScope _p(st, K_MISC, 0.0);
+        count_launch(K_MISC);
+        gather_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, si, P, lr.w.gath, mp, lr.w.Yfull, ni);
+        RUTV_LAUNCH_CK();
+      }
+      apply_left(lr, lr.V, lr.ldv, lr.nl, si, ni, b, lr.w.Yfull, ni, lr.w.Tv_all + size_t(si) * b * b, b);
+      apply_left(lr, lr.U, lr.ldu, local_cols(m, b, lr.r, P), si, mi, b, lr.w.Wu_all + plan_.off_u[si], mi,
+                 lr.w.Tu_all + size_t(si) * b * b, b);
+    }
+  }
+  // column folds with the small SVD factors, on the owner of each block
+  auto fold_cols = [&](LocalRank& lr, double* X, int64_t rows, int64_t ldx, int64_t p, int64_t k, const double* F) {
+    double* Xb = X + b * blocks_before(p, lr.r, P) * ldx;
+    dg(lr.w, st, false, false, rows, k, k, 1.0, Xb, ldx, F, k, 0.0, lr.w.fold, rows);
+    copy_matrix(st, rows, k, lr.w.fold, rows, Xb, ldx);
+  };
+  for (int64_t si = 0; si < steps; ++si)
+    for (auto& lr : L) {
+      if (int(si % P) != lr.r) continue;
+      const int64_t js = si / P;
+      fold_cols(lr, lr.U, m, lr.ldu, si, b, lr.w.Usall + size_t(js) * b * b);
+      fold_cols(lr, lr.V, n, lr.ldv, si, b, lr.w.Vsall + size_t(js) * b * b);
+    }
+  if (final_block)
+    for (auto& lr : L) {
+      if (int(pf % P) != lr.r) continue;
+      fold_cols(lr, lr.U, m, lr.ldu, pf, nif, lr.w.Usfin);
+      fold_cols(lr, lr.V, n, lr.ldv, pf, nif, lr.w.Vsfin);
+    }
+  (void)r0f;
 }
 
 std::mutex g_dmu;
@@ -982,7 +1130,8 @@ int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_t rank, int3
 
 int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m, int64_t n, const double* const* A_loc,
                         const int64_t* lda_loc, int64_t b, int32_t q, uint64_t seed, int64_t k_stop,
-                        double* const* T_loc, const int64_t* ldt_loc, randutv_info* info) {
+                        double* const* U_loc, const int64_t* ldu_loc, double* const* T_loc, const int64_t* ldt_loc,
+                        double* const* V_loc, const int64_t* ldv_loc, randutv_info* info) {
   if (!comm) return -2;
   if (m < 1) return -3;
   if (n < 1 || n > m) return -4;
@@ -990,7 +1139,10 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   if (b < 1 || b > RANDUTV_MAX_B) return -7;
   if (q < 0) return -8;
   if (k_stop < 0) return -10;
-  if (!T_loc || !ldt_loc) return -11;
+  if (!T_loc || !ldt_loc) return -13;
+  const bool uv = (U_loc != nullptr);
+  if (uv && !ldu_loc) return -12;
+  if (uv != (V_loc != nullptr) || (V_loc && !ldv_loc)) return -16;
   randutv_opts o{};
   if (opts) o = *opts;
   if (o.tol < 0 || std::isnan(o.tol) || o.qr_mode < 0 || o.qr_mode > 1 || o.oversample < 0) return -1;
@@ -1001,11 +1153,13 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   for (int l = 0; l < nlr; ++l) {
     const int64_t nl = local_cols(n, b, c.ranks[l], c.P);
     if (nl > 0 && (!A_loc[l] || lda_loc[l] < m)) return -5;
-    if (nl > 0 && (!T_loc[l] || ldt_loc[l] < m)) return -11;
+    if (nl > 0 && (!T_loc[l] || ldt_loc[l] < m)) return -13;
+    if (uv && local_cols(m, b, c.ranks[l], c.P) > 0 && (!U_loc[l] || ldu_loc[l] < m)) return -12;
+    if (uv && nl > 0 && (!V_loc[l] || ldv_loc[l] < n)) return -16;
   }
   std::lock_guard<std::mutex> lock(rutv::g_dmu);
   try {
-    rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P);
+    rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P, uv);
     const size_t per = rutv::dist_rank_bytes(d);
     char* ws = (char*)rutv::dist_ws(per * nlr);
     if (!ws) return RANDUTV_ERR_NOMEM;
@@ -1017,6 +1171,10 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
       lr.lda = lda_loc[l];
       lr.T = T_loc[l];
       lr.ldt = ldt_loc[l];
+      lr.U = uv ? U_loc[l] : nullptr;
+      lr.V = uv ? V_loc[l] : nullptr;
+      lr.ldu = uv ? ldu_loc[l] : 0;
+      lr.ldv = uv ? ldv_loc[l] : 0;
       lr.nl = local_cols(n, b, lr.r, c.P);
       rutv::Arena ar;
       ar.base = ws + per * l;
@@ -1027,7 +1185,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
     }
     // optimistic first (no per-panel host synchronisation; run() falls back to
     // the synchronous mode on every rank if any rank factors in place)
-    rutv::DistFactor f(c, o, m, n, b, q, seed, k_stop, L);
+    rutv::DistFactor f(c, o, m, n, b, q, seed, k_stop, L, d);
     int rc = f.run(info, true);
     if (rc == rutv::kDistRetry) rc = f.run(info, false);
     return rc;

@@ -33,6 +33,8 @@ def _lib():
         L.randutv_dist_global_col.restype = c_i64
         L.randutv_factor_dist.argtypes = [ctypes.POINTER(_Opts), c_vp, c_i64, c_i64, ctypes.POINTER(c_vp),
                                           ctypes.POINTER(c_i64), c_i64, c_i32, ctypes.c_uint64, c_i64,
+                                          ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
+                                          ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
                                           ctypes.POINTER(c_vp), ctypes.POINTER(c_i64), ctypes.POINTER(_Info)]
         for f in ("randutv_nccl_unique_id", "randutv_comm_init_nccl", "randutv_comm_init_loopback",
                   "randutv_comm_destroy", "randutv_comm_local_ranks", "randutv_factor_dist"):
@@ -140,10 +142,12 @@ def nccl_from_torch(group=None) -> Comm:
 
 # --------------------------------------------------------------------------- the factorization
 def factor(comm: Comm, shards, m: int, n: int, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
-           reortho: bool = True, qr_mode: int = 0, out=None, stream=None):
-    """Distributed A = U T V^T, T-only.  ``shards``: one column-major CUDA
-    tensor per rank driven by ``comm`` (comm.ranks order), rank r's shard being
-    m x local_cols(n, b, r, P).  Returns (T shards, Info)."""
+           reortho: bool = True, qr_mode: int = 0, out=None, stream=None, with_uv: bool = False):
+    """Distributed A = U T V^T.  ``shards``: one column-major CUDA tensor per
+    rank driven by ``comm`` (comm.ranks order), rank r's shard being
+    m x local_cols(n, b, r, P).  Returns (T shards, Info), or with ``with_uv``
+    (U shards, T shards, V shards, Info) -- U's shard of rank r is
+    m x local_cols(m, b, r, P), V's n x local_cols(n, b, r, P)."""
     L = _lib()
     nl = len(comm.ranks)
     assert len(shards) == nl, "one shard per local rank"
@@ -154,11 +158,25 @@ def factor(comm: Comm, shards, m: int, n: int, b: int, q: int, seed: int, k_stop
     lda = (c_i64 * nl)(*[_ld(S) for S in shards])
     Tp = (c_vp * nl)(*[T.data_ptr() for T in out])
     ldt = (c_i64 * nl)(*[_ld(T) for T in out])
+    Up = Vp = ldu = ldv = None
+    if with_uv:
+        bb = min(int(b), n)
+        Us = [empty_cm(m, max(local_cols(m, bb, r, comm.world), 1), S.device) for r, S in zip(comm.ranks, shards)]
+        Vs = [empty_cm(n, max(local_cols(n, bb, r, comm.world), 1), S.device) for r, S in zip(comm.ranks, shards)]
+        Up = (c_vp * nl)(*[U.data_ptr() for U in Us])
+        Vp = (c_vp * nl)(*[V.data_ptr() for V in Vs])
+        ldu = (c_i64 * nl)(*[_ld(U) for U in Us])
+        ldv = (c_i64 * nl)(*[_ld(V) for V in Vs])
     opts = _Opts(stream=_stream(stream, shards[0].device).value, tol=float(tol), no_reortho=0 if reortho else 1,
                  qr_mode=int(qr_mode))
     info = _Info()
     rc = L.randutv_factor_dist(ctypes.byref(opts), comm.h, m, n, Ap, lda, int(b), int(q), int(seed) & (2**64 - 1),
-                               int(k_stop), Tp, ldt, ctypes.byref(info))
+                               int(k_stop), Up, ldu, Tp, ldt, Vp, ldv, ctypes.byref(info))
     _check(rc, "randutv_factor_dist")
-    return out, Info(info.k_done, info.steps, bool(info.final_block), info.max_sweeps, info.trailing_fro,
-                     info.a_fro, info.qr_fallbacks)
+    inf = Info(info.k_done, info.steps, bool(info.final_block), info.max_sweeps, info.trailing_fro, info.a_fro,
+               info.qr_fallbacks)
+    if with_uv:
+        Us = [U[:, :local_cols(m, min(int(b), n), r, comm.world)] for r, U in zip(comm.ranks, Us)]
+        Vs = [V[:, :local_cols(n, min(int(b), n), r, comm.world)] for r, V in zip(comm.ranks, Vs)]
+        return Us, out, Vs, inf
+    return out, inf

@@ -119,3 +119,43 @@ def test_dist_nccl_one_rank():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def run_dist_uv(A, nranks, b, q, seed, **kw):
+    m, n = A.shape
+    comm = D.loopback(nranks)
+    Ad = to_dev(A)
+    shards = [D.shard(Ad, b, r, nranks) for r in range(nranks)]
+    Us, Ts, Vs, info = D.factor(comm, shards, m, n, b, q, seed, with_uv=True, **kw)
+    torch.cuda.synchronize()
+    comm.close()
+    bb = min(b, n)
+    U = D.assemble(Us, m, bb).cpu().numpy()
+    T = D.assemble(Ts, n, bb).cpu().numpy()
+    V = D.assemble(Vs, n, bb).cpu().numpy()
+    return U, T, V, info
+
+
+@pytest.mark.parametrize("m,n,b,q,nranks,kw", [
+    (500, 500, 50, 1, 3, {}),                      # c1 shape
+    (1000, 400, 64, 1, 2, {}),                     # tall: final tall block (QR + SVD)
+    (333, 150, 64, 2, 4, {}),                      # ragged, a rank without V columns
+    (600, 600, 64, 1, 3, {"k_stop": 192}),         # early stop: dense trailing block
+    (384, 384, 128, 0, 2, {"qr_mode": 1}),         # Householder panels
+])
+def test_dist_uv_factorization(m, n, b, q, nranks, kw):
+    """U and V formed on the shards (backward accumulation):
+    A = U T V^T and orthogonality to the north star's 1e-13 n bound; T as in the
+    T-only run against the oracle."""
+    A = testmat.gaussian(m, n, m + n + nranks)
+    U, T, V, info = run_dist_uv(A, nranks, b, q, 7, **kw)
+    a = np.linalg.norm(A)
+    assert np.linalg.norm(A - U @ T @ V.T) <= 1e-13 * n * a
+    assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-13 * n
+    assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-13 * n
+    ref = oracle.randutv(A, b, q, 7, build_ortho=False, **{k: v for k, v in kw.items() if k == "k_stop"})
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    # the T-only distributed run gives the same T to rounding
+    T0, _ = run_dist(A, nranks, b, q, 7, **kw)
+    np.testing.assert_allclose(T, T0, rtol=0, atol=1e-12 * a)
