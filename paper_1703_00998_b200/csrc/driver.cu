@@ -540,6 +540,10 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     info->qr_fallbacks = fallbacks;
     info->max_sweeps = 0;
     for (int v : sw) info->max_sweeps = std::max(info->max_sweeps, v);
+    if (getenv("RANDUTV_DEBUG_SWEEPS")) {  // diagnostics only
+      for (int v : sw) fprintf(stderr, "%d ", v);
+      fprintf(stderr, "\n");
+    }
   }
   (void)trailing;
   return RANDUTV_OK;

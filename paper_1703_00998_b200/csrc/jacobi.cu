@@ -252,7 +252,211 @@ jacobi_cluster_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm,
   }
 }
 
-// sigma_j = ||B(:,j)||, sort descending, Us = W(:,perm), Vs = B(:,perm)/sigma.
+// ---- k <= 256: cross-pair block ordering, one register-resident column per warp
+//
+// Same tournament over blocks of 16 columns as jacobi_cluster_k, but a round
+// visits only the 256 CROSS pairs of its block pair (16 sub-rounds, pair
+// (w, (w + sh) mod 16)), and the within-block pairs are visited once per sweep
+// (round 0, all blocks at once): every column pair exactly once per sweep, as
+// in a cyclic sweep, instead of the within-block pairs once per round (1.8x
+// the pair visits; simulated on the c3 R11 blocks: same sweep count).  Warp w
+// keeps column w of the first block (B and W) in registers for the whole
+// round; the second block lives in shared memory and each of its columns is
+// read, rotated and written back by one warp per sub-round.  Column norms are
+// recomputed for every pair (alpha, beta, gamma in one fused warp reduction):
+// on the c3 blocks (150 singular values within 1e-10 of each other) the
+// tracked norms of Rutishauser's update cost extra sweeps.
+// Lane l holds rows 64e + 2l + {0, 1} (e < EPL/2): 16-byte shared accesses.
+template <int EPL>
+struct JacCol {
+  double v[EPL];
+};
+
+template <int EPL>
+__device__ __forceinline__ void jc_lds(JacCol<EPL>& c, const double* col, int lane) {
+#pragma unroll
+  for (int e = 0; e < EPL / 2; ++e) {
+    const double2 t = *reinterpret_cast<const double2*>(col + 64 * e + 2 * lane);
+    c.v[2 * e] = t.x;
+    c.v[2 * e + 1] = t.y;
+  }
+}
+template <int EPL>
+__device__ __forceinline__ void jc_sts(double* col, const JacCol<EPL>& c, int lane) {
+#pragma unroll
+  for (int e = 0; e < EPL / 2; ++e)
+    *reinterpret_cast<double2*>(col + 64 * e + 2 * lane) = make_double2(c.v[2 * e], c.v[2 * e + 1]);
+}
+
+// 1/x for x > 0 normal: MUFU seed + two Newton steps (relative error ~1e-16;
+// the rotation stays orthogonal to rounding whatever the accuracy of t, since
+// c = (1 + t^2)^-1/2 and s = c t)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// rotate (x, y) so that x^T y = 0; returns 1 if a rotation was applied.
+// alpha, beta, gamma by one transposed warp reduction (lane L ends with the
+// total of value L & 3); t = 2 gamma sgn(d) / (|d| + sqrt(d^2 + 4 gamma^2)),
+// d = beta - alpha -- the classical t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+// zeta = d / (2 gamma), with one reciprocal and no overflow for small gamma.
+template <int EPL>
+__device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCol<EPL>& xw, JacCol<EPL>& yw,
+                                         double tol) {
+  const int lane = threadIdx.x & 31;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    v[0] = fma(xb.v[e], xb.v[e], v[0]);
+    v[1] = fma(yb.v[e], yb.v[e], v[1]);
+    v[2] = fma(xb.v[e], yb.v[e], v[2]);
+  }
+  {  // 4 values x 32 lanes: 2 transposed levels, then 3 plain levels
+    const bool u2 = (lane & 2) != 0;
+    double s0 = u2 ? v[0] : v[2], s1 = u2 ? v[1] : v[3];
+    double k0 = u2 ? v[2] : v[0], k1 = u2 ? v[3] : v[1];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    const bool u1 = (lane & 1) != 0;
+    double s = u1 ? k0 : k1, k = u1 ? k1 : k0;
+    k += __shfl_xor_sync(0xffffffffu, s, 1);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    v[0] = k;
+  }
+  const double al = __shfl_sync(0xffffffffu, v[0], 0);
+  const double be = __shfl_sync(0xffffffffu, v[0], 1);
+  const double ga = __shfl_sync(0xffffffffu, v[0], 2);
+  if (!(ga != 0.0 && fabs(ga) > tol * sqrt(al * be))) return 0;
+  const double d = be - al, g2 = 2.0 * ga;
+  const double h = fma(d, d, g2 * g2);
+  const double root = h * rsqrt(h);
+  const double t = (d >= 0.0 ? g2 : -g2) * rcp_fast(fabs(d) + root);
+  const double c = rsqrt(fma(t, t, 1.0));
+  const double s = c * t;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const double x = xb.v[e], y = yb.v[e];
+    xb.v[e] = c * x - s * y;
+    yb.v[e] = s * x + c * y;
+    const double u = xw.v[e], w = yw.v[e];
+    xw.v[e] = c * u - s * w;
+    yw.v[e] = s * u + c * w;
+  }
+  return 1;
+}
+
+template <int EPL>
+__global__ void __launch_bounds__(JNT)
+jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts,
+                  double tol) {
+  constexpr int KB = 16, KP = 32 * EPL;  // block width, padded column length
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double js[];
+  double* sB = js;  // [2 KB][KP]: block p (cols 0..15), block q (16..31)
+  double* sW = js + 2 * KB * KP;
+  __shared__ int rot_sm;
+  const int mat = blockIdx.y;
+  const int cta = (int)cluster.block_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* cnt = counts + mat * (MAX_SWEEPS + 1);
+  const int k = d.k;
+  double* B = Bw + int64_t(mat) * k * k;
+  double* W = Wm + int64_t(mat) * k * k;
+  // global <-> shared for one block (16 columns, zero padding beyond k)
+  auto load_block = [&](int blk, int slot) {
+    for (int idx = threadIdx.x; idx < KB * KP; idx += JNT) {
+      const int c = idx / KP, r = idx % KP, g = blk * KB + c;
+      const bool ok = g < k && r < k;
+      sB[(slot * KB + c) * KP + r] = ok ? __ldcg(B + r + int64_t(g) * k) : 0.0;
+      sW[(slot * KB + c) * KP + r] = ok ? __ldcg(W + r + int64_t(g) * k) : 0.0;
+    }
+  };
+  auto store_block = [&](int blk, int slot) {
+    for (int idx = threadIdx.x; idx < KB * KP; idx += JNT) {
+      const int c = idx / KP, r = idx % KP, g = blk * KB + c;
+      if (g < k && r < k) {
+        __stcg(B + r + int64_t(g) * k, sB[(slot * KB + c) * KP + r]);
+        __stcg(W + r + int64_t(g) * k, sW[(slot * KB + c) * KP + r]);
+      }
+    }
+  };
+  for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+    if (threadIdx.x == 0) rot_sm = 0;
+    int rot = 0;
+    for (int round = 0; round < d.nb - 1; ++round) {
+      int bp, bq;
+      rr_pair(d.nb, round, cta, bp, bq);
+      load_block(bp, 0);
+      load_block(bq, 1);
+      __syncthreads();
+      if (round == 0) {
+        // within-block pairs of both blocks: warp w -> block w / 8, pair w % 8
+        const int slot = warp >> 3, pi = warp & 7;
+        for (int sr = 0; sr < KB - 1; ++sr) {
+          int p, q;
+          rr_pair(KB, sr, pi, p, q);
+          double* cbp = sB + (slot * KB + p) * KP;
+          double* cbq = sB + (slot * KB + q) * KP;
+          double* cwp = sW + (slot * KB + p) * KP;
+          double* cwq = sW + (slot * KB + q) * KP;
+          JacCol<EPL> xb, yb, xw, yw;
+          jc_lds(xb, cbp, lane);
+          jc_lds(yb, cbq, lane);
+          jc_lds(xw, cwp, lane);
+          jc_lds(yw, cwq, lane);
+          if (jc_rotate(xb, yb, xw, yw, tol)) {
+            jc_sts(cbp, xb, lane);
+            jc_sts(cbq, yb, lane);
+            jc_sts(cwp, xw, lane);
+            jc_sts(cwq, yw, lane);
+            ++rot;
+          }
+          __syncthreads();
+        }
+      }
+      // cross pairs: warp w holds column w of block p
+      JacCol<EPL> xb, xw;
+      jc_lds(xb, sB + warp * KP, lane);
+      jc_lds(xw, sW + warp * KP, lane);
+      for (int sh = 0; sh < KB; ++sh) {
+        const int q = KB + ((warp + sh) & (KB - 1));
+        double* cbq = sB + q * KP;
+        double* cwq = sW + q * KP;
+        JacCol<EPL> yb, yw;
+        jc_lds(yb, cbq, lane);
+        jc_lds(yw, cwq, lane);
+        if (jc_rotate(xb, yb, xw, yw, tol)) {
+          jc_sts(cbq, yb, lane);
+          jc_sts(cwq, yw, lane);
+          ++rot;
+        }
+        __syncthreads();
+      }
+      jc_sts(sB + warp * KP, xb, lane);
+      jc_sts(sW + warp * KP, xw, lane);
+      __syncthreads();
+      store_block(bp, 0);
+      store_block(bq, 1);
+      __threadfence();
+      cluster.sync();
+    }
+    if (lane == 0 && rot) atomicAdd(&rot_sm, rot);
+    __syncthreads();
+    if (threadIdx.x == 0 && rot_sm) atomicAdd(&cnt[sweep + 1], rot_sm);
+    __threadfence();
+    cluster.sync();
+    const int total = atomicAdd(&cnt[sweep + 1], 0);
+    if (total == 0) break;
+  }
+}
+
+// sigma_j = ||B(:,j)||, sort descending, Us = W(:,perm), Vs = B(:,perm) / sigma.
 __global__ void __launch_bounds__(JNT)
 jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict__ Wm, double* __restrict__ D,
                   double* __restrict__ Us, double* __restrict__ Vs, const int* __restrict__ counts,
@@ -391,7 +595,33 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
   const double tol = double(k) * DBL_EPSILON;
   const int csize = d.nb / 2;
-  if (k > 1 && csize <= MAX_CLUSTER) {
+  if (k > 1 && k <= 256 && d.kb == 16) {
+    const int epl = k <= 64 ? 2 : (k <= 128 ? 4 : 8);
+    const size_t smem2 = size_t(2) * 2 * 16 * 32 * epl * sizeof(double);
+    auto kern = epl == 2 ? jacobi_cluster2_k<2> : (epl == 4 ? jacobi_cluster2_k<4> : jacobi_cluster2_k<8>);
+    static bool attr2[3] = {false, false, false};
+    const int ai = epl == 2 ? 0 : (epl == 4 ? 1 : 2);
+    if (!attr2[ai]) {
+      RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2[ai] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize, batch, 1);
+    cfg.blockDim = dim3(JNT, 1, 1);
+    cfg.dynamicSmemBytes = smem2;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope _p(st, K_SVD, 0.0);
+    count_launch(K_SVD);
+    RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, Bw, Wm, counts, tol));
+  } else if (k > 1 && csize <= MAX_CLUSTER) {
+
     // one cluster per matrix runs every round and sweep in-kernel
     static size_t attr_c = 0;
     if (smem > attr_c) {
