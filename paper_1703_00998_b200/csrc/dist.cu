@@ -687,7 +687,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           SmallWork sw = lr.sw;
           int* f = opt_ ? next_flag(l) : nullptr;
           if (f) sw.flag = f;
-          small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b);
+          small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b, lr.w.part, lr.w.part_elems);
         }
         qr_ok = opt_ ? true : (read_int_sync(st, L[0].sw.flag) == 0);
         if (qr_ok) {

@@ -91,7 +91,7 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w);
 // W2 = Q1^T Q1 -> second pass + Householder reconstruction: writes R (b x b,
 // ld ldr), tau, Tw (ld ldt), w.M = R2^-1 U~^-1 and w.F (L strictly below), w.flag.
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
-                 int64_t ldr, double* tau, double* Tw, int64_t ldt);
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems);
 // V(0:b, 0:b) <- unit lower L from w.F
 void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv);
 

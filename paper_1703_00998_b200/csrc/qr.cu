@@ -512,7 +512,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems);      // G2
     const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
-    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt);
+    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems);
     if (optimistic || read_flag_sync(st, sw.flag) == 0) {
       if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
         dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems, 0,

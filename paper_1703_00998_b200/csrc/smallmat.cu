@@ -23,6 +23,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cfloat>
 
 #include "common.cuh"
@@ -51,6 +53,8 @@ struct SmallSm {
   double aug[TS * 97];               // row-major augmented elimination work area [32][96] (+1 pad)
   double piv[TS];
   double sgn[TS];
+  double rowbuf[2][96];  // pivot row of the current column step (double-buffered)
+  double colbuf[2][TS];  // pivot column of the current column step
   double dmin, dmax;
   unsigned long long devbits;  // cluster max |G2 - I| (bit pattern of a non-negative double)
   int bad;
@@ -196,27 +200,84 @@ __device__ void tile_sum(double (&acc)[2][2], int np, GP gp, SmallSm& s) {
 // In: G tile (column-major in s.d, upper triangle read).  Out: s.d = R (zeros
 // below), s.di = R^-1, s.dit = R^-T.  Non-positive / non-finite pivots of valid
 // columns set s.bad (and are replaced by 1).
+// 1/x for finite x != 0: MUFU seed + two Newton steps (~1 ulp; the division
+// routine's slow-path checks sat on the per-column critical path)
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// publish row k and column k (k < 32) of a register-resident augmented
+// matrix (thread owns row i, columns j0 .. j0 + N - 1) for the next column step
+// The row buffer is stored permuted: the 16-byte chunk jj/2 of the 8 column
+// groups are adjacent, so the 8 lanes of a row reading (or writing) their
+// chunk touch 128 contiguous bytes (the natural layout's 64- or 96-byte
+// stride between groups made every 16-byte access a 4-way bank conflict:
+// 484 -> 326 cycles per column step, tools/scratch/stepbench.cu)
+template <int N>
+__device__ __forceinline__ int rb_pos(int j) {
+  const int g = j / N, jj = j % N;
+  return (jj >> 1) * 16 + g * 2 + (jj & 1);
+}
+template <int N>
+__device__ __forceinline__ void aug_publish(SmallSm& s, const double (&a)[N], int i, int j0, int k, int buf) {
+  (void)j0;
+  if (i == k) {
+#pragma unroll
+    for (int jj = 0; jj < N; jj += 2)
+      *reinterpret_cast<double2*>(&s.rowbuf[buf][(jj >> 1) * 16 + (threadIdx.x & 7) * 2]) =
+          make_double2(a[jj], a[jj + 1]);
+  }
+  // owner of column k: j0 = N (k / N); k is an unrolled loop index at every
+  // call site, so a[k % N] is a static register
+  if ((threadIdx.x & 7) == k / N) s.colbuf[buf][i] = a[k % N];
+}
+
 __device__ __noinline__ void cta_chol_inv(SmallSm& s, int gcol0, int b) {
   constexpr int LD = 65;
   double* A = s.aug;
   const int tid = threadIdx.x;
-  for (int e = tid; e < TS * 64; e += SNT) {
-    const int i = e >> 6, j = e & 63;
-    A[i * LD + j] = (j < TS) ? s.d[max(i, j) * SLD + min(i, j)] : ((j - TS == i) ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  for (int k = 0; k < TS; ++k) {
-    double p = A[k * LD + k];
-    if (!(p > 0.0) || !isfinite(p)) p = 1.0;  // flagged below from the stored pivot
-    const double invp = 1.0 / p;
-    const double* rowk = A + k * LD;
+  // thread t owns row i = t / 8, columns 8 (t % 8) .. +7 of [G | I] in
+  // registers for all 32 column steps; per step only the pivot row and column
+  // go through shared memory (published by their owners, double-buffered), so
+  // a step is one barrier, ~6 shared loads and 8 FMAs per thread
+  const int i = tid >> 3, j0 = (tid & 7) * 8;
+  double a[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * SNT, i = e >> 6, j = e & 63;
-      if (i > k && j > k) A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = j0 + jj;
+    a[jj] = (j < TS) ? s.d[max(i, j) * SLD + min(i, j)] : ((j - TS == i) ? 1.0 : 0.0);
+  }
+  aug_publish(s, a, i, j0, 0, 0);
+  __syncthreads();
+#pragma unroll  // k - j0 must be a compile-time register index in aug_publish
+  for (int k = 0; k < TS; ++k) {
+    const int buf = k & 1;
+    double p = s.rowbuf[buf][rb_pos<8>(k)];
+    if (!(p > 0.0) || !isfinite(p)) p = 1.0;  // flagged below from the stored pivot
+    if (i > k) {
+      const double l = s.colbuf[buf][i] * frcp(p);
+      double r[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; jj += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(&s.rowbuf[buf][(jj >> 1) * 16 + (tid & 7) * 2]);
+        r[jj] = t.x;
+        r[jj + 1] = t.y;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (j0 + jj > k) a[jj] = fma(-l, r[jj], a[jj]);
     }
+    if (k + 1 < TS) aug_publish(s, a, i, j0, k + 1, buf ^ 1);
     __syncthreads();
   }
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) A[i * LD + j0 + jj] = a[jj];
+  __syncthreads();
   if (tid < TS) {
     double p = A[tid * LD + tid];
     const bool ok = (p > 0.0) && isfinite(p);
@@ -258,35 +319,67 @@ __device__ __noinline__ void cta_lu_sign_inv(SmallSm& s) {
   constexpr int LD = 97;
   double* A = s.aug;
   const int tid = threadIdx.x;
-  for (int e = tid; e < TS * 96; e += SNT) {
-    const int i = e / 96, j = e - i * 96;
-    A[i * LD + j] = (j < TS) ? s.d[j * SLD + i] : (((j - TS) & 31) == i ? 1.0 : 0.0);
-  }
+  // register-resident rows: thread t owns row i = t / 8 and, in each of the
+  // three 32-column regions of [F | I | I], the 4 columns 4 (t % 8) .. +3, so
+  // the kind of update of a register is known at compile time.  Row buffer
+  // position of column j (region r, c = j mod 32, group c / 4, q = c mod 4):
+  // chunk 2r + q/2 of 16 doubles (8 groups x 2), conflict-free 16-byte access.
+  const int i = tid >> 3, g = tid & 7;
+  auto pos = [](int j) { const int r = j >> 5, c = j & 31, q = c & 3; return (2 * r + (q >> 1)) * 16 + (c >> 2) * 2 + (q & 1); };
+  double a[12];  // a[4 r + q] = A(i, 32 r + 4 g + q)
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = 4 * g + q;
+      a[4 * r + q] = (r == 0) ? s.d[c * SLD + i] : (c == i ? 1.0 : 0.0);
+    }
+  auto publish = [&](int k, int buf) {  // row k, column k (region 0) for the next step
+    if (i == k) {
+#pragma unroll
+      for (int h = 0; h < 6; ++h)
+        *reinterpret_cast<double2*>(&s.rowbuf[buf][h * 16 + g * 2]) = make_double2(a[2 * h], a[2 * h + 1]);
+    }
+    if (g == (k >> 2)) s.colbuf[buf][i] = a[k & 3];
+  };
+  publish(0, 0);
   __syncthreads();
+#pragma unroll  // k & 3 must be a compile-time register index
   for (int k = 0; k < TS; ++k) {
-    const double a = A[k * LD + k];
-    const double sg = (a <= 0.0) ? -1.0 : 1.0;
-    const double pv = a + sg;
-    const double invp = 1.0 / pv;
+    const int buf = k & 1;
+    const double av = s.rowbuf[buf][pos(k)];
+    const double sg = (av <= 0.0) ? -1.0 : 1.0;
+    const double pv = av + sg;
     if (tid == 0) {
       s.sgn[k] = sg;
       s.piv[k] = pv;
     }
-    const double* rowk = A + k * LD;
+    if (i > k) {
+      const double invp = frcp(pv);
+      const double l = s.colbuf[buf][i] * invp;         // F and L^-1 regions: A(i,k) / pivot
+      const double lu = s.rowbuf[buf][pos(i)] * invp;   // U~^T region: A(k,i) / pivot
+      double rv[12];
 #pragma unroll
-    for (int u = 0; u < 12; ++u) {
-      const int e = tid + u * SNT, i = e / 96, j = e - i * 96;
-      if (i <= k) continue;
-      if (j < TS) {
-        if (j > k) A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
-      } else if (j < 2 * TS) {
-        A[i * LD + j] = fma(-A[i * LD + k] * invp, rowk[j], A[i * LD + j]);
-      } else {
-        A[i * LD + j] = fma(-rowk[i] * invp, rowk[j], A[i * LD + j]);
+      for (int h = 0; h < 6; ++h) {
+        const double2 t = *reinterpret_cast<const double2*>(&s.rowbuf[buf][h * 16 + g * 2]);
+        rv[2 * h] = t.x;
+        rv[2 * h + 1] = t.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * g + q > k) a[q] = fma(-l, rv[q], a[q]);
+        a[4 + q] = fma(-l, rv[4 + q], a[4 + q]);
+        a[8 + q] = fma(-lu, rv[8 + q], a[8 + q]);
       }
     }
+    if (k + 1 < TS) publish(k + 1, buf ^ 1);
     __syncthreads();
   }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) A[i * LD + 32 * r + 4 * g + q] = a[4 * r + q];
+  __syncthreads();
   if (tid < TS) s.c[tid] = 1.0 / s.piv[tid];
   __syncthreads();
   const double* rp = s.c;
@@ -394,8 +487,11 @@ __device__ void lu_sign_inv_dev(cg::cluster_group& cl, const SmallDims& d, doubl
   const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
   const int bp = d.bp, nb = d.nb;
   for (int p = 0; p < nb; ++p) {
+    SMALL_MARK(0);
     tile_load_sync(s.d, TRef{tile_ptr(F, bp, p, p), bp, 0});
+    SMALL_MARK(1);
     cta_lu_sign_inv(s);
+    SMALL_MARK(2);
     if (cta == 0) {
       copy_tile_smem_to_global(s.d, tile_ptr(F, bp, p, p), bp);
       copy_tile_smem_to_global(s.di, tile_ptr(Li, bp, p, p), bp);
@@ -442,7 +538,9 @@ __device__ void lu_sign_inv_dev(cg::cluster_group& cl, const SmallDims& d, doubl
       }
       __syncthreads();
     }
+    SMALL_MARK(3);
     cluster_barrier(cl);
+    SMALL_MARK(4);
     const int nt = nr * nr;
     for (int task = cta; task < nt; task += C) {
       const int i = p + 1 + task % nr, j = p + 1 + task / nr;
@@ -454,6 +552,7 @@ __device__ void lu_sign_inv_dev(cg::cluster_group& cl, const SmallDims& d, doubl
       acc_sub_global(acc, tile_ptr(F, bp, i, j), bp);
       __syncthreads();
     }
+    SMALL_MARK(5);
     cluster_barrier(cl);
   }
 }
@@ -520,18 +619,20 @@ struct ReconArgs {
   double dev_max;                                // max |G2 - I| accepted
 };
 
-// kernel 2: second CholeskyQR pass + Householder reconstruction.
-__global__ void __launch_bounds__(SNT, 1) recon_k(ReconArgs a) {
+// kernel 2a: second CholeskyQR pass (R2, R2^-1) and the validity flag.
+// Also zero-pads F (written by the b x b GEMM F = -Q(0:b,:) R2^-1 next) and
+// zeroes the strictly-lower tiles of R2, R2^-1.
+__global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
   __shared__ double devred[SNT / 32];
   const SmallDims d = a.d;
   const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
-  const int bp = d.bp, nb = d.nb, b = d.b;
+  const int bp = d.bp, b = d.b;
   init_stats(s);
   cl.sync();  // every CTA's stats are initialised before any remote update
-  // ---- init: deviation of G2 from I (before padding), padding, zero lower tiles, padded Q block
+  // ---- deviation of G2 from I (before padding), padding, zero lower tiles
   {
     double dev = 0.0;
     const int64_t tot = int64_t(bp) * bp;
@@ -542,16 +643,12 @@ __global__ void __launch_bounds__(SNT, 1) recon_k(ReconArgs a) {
         dev = fmax(dev, isfinite(v) ? fabs(v) : 1e300);
       } else {
         a.W2[e] = (r == c) ? 1.0 : 0.0;
+        a.F[e] = 0.0;
       }
-      a.F[e] = (r < b && c < b) ? a.Q1[r + c * a.ldq] : 0.0;  // F <- Q block (negated in the first phase)
       if (r / TS > c / TS) {
         a.R2[e] = 0.0;
         a.R2i[e] = 0.0;
-        a.Ui[e] = 0.0;
-        a.M[e] = 0.0;
-        a.US[e] = 0.0;
       }
-      if (r / TS < c / TS) a.Li[e] = 0.0;
     }
     for (int o = 16; o; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
     if ((threadIdx.x & 31) == 0) devred[threadIdx.x >> 5] = dev;
@@ -566,8 +663,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_k(ReconArgs a) {
     __syncthreads();
   }
   cluster_barrier(cl);
-  // ---- second Cholesky pass.  G2 = Q1^T Q1 = I + E: when b max|E| <= 1e-8 the
-  // factor and its inverse are, to O((b max|E|)^2) <= 1e-16,
+  // ---- G2 = Q1^T Q1 = I + E: when b max|E| <= 1e-8 the factor and its inverse
+  // are, to O((b max|E|)^2) <= 1e-16,
   //   R2 = I + U(E),  R2^-1 = I - U(E),  U(E) = striu(E) + diag(E)/2
   // (R2^T R2 = I + U + U^T + O(E^2) = I + E), so the 8-step Cholesky is skipped.
   const double devmax = __longlong_as_double((long long)*cl.map_shared_rank(&s.devbits, 0));
@@ -580,101 +677,54 @@ __global__ void __launch_bounds__(SNT, 1) recon_k(ReconArgs a) {
       a.R2[e] = (r == c ? 1.0 : 0.0) + u;
       a.R2i[e] = (r == c ? 1.0 : 0.0) - u;
     }
-    cluster_barrier(cl);
   } else {
     chol_inv_dev(cl, d, a.W2, a.R2, a.R2i, s);
   }
-  // ---- F = -(Q(0:b, :) R2^-1)   (F currently holds the padded Q block; use US as the source copy)
-  {
-    // copy F -> US (source), then F(I,J) = -sum_{K<=J} US(I,K) R2i(K,J)
-    const int64_t tot = int64_t(bp) * bp;
-    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) a.US[e] = a.F[e];
-    cluster_barrier(cl);
-    for (int task = cta; task < nb * nb; task += C) {
-      const int I = task % nb, J = task / nb;
-      double acc[2][2];
-      tile_sum(acc, J + 1, [&](int q, TRef& A, TRef& B) {
-        A = TRef{tile_ptr(a.US, bp, I, q), bp, 0};
-        B = TRef{tile_ptr(a.R2i, bp, q, J), bp, 0};
-      }, s);
-      acc_to_global(acc, tile_ptr(a.F, bp, I, J), bp, -1.0);
-      __syncthreads();
-    }
-    cluster_barrier(cl);
-    // US is reused below: clear its lower tiles again
-    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-      const int r = int(e % bp), c = int(e / bp);
-      if (r / TS > c / TS) a.US[e] = 0.0;
-    }
-  }
-  // ---- sign-modified LU with inverses
-  lu_sign_inv_dev(cl, d, a.F, a.Li, a.Ui, a.S, s);
-  // ---- US = U~ S (upper tiles; lower part of diagonal tiles zeroed)
-  {
-    const int64_t tot = int64_t(bp) * bp;
-    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-      const int r = int(e % bp), c = int(e / bp);
-      if (r / TS <= c / TS) a.US[e] = (r <= c) ? __ldcg(a.F + e) * __ldcg(a.S + c) : 0.0;
-    }
-  }
-  cluster_barrier(cl);
-  // ---- T = US Li^T, M = R2i Ui, Rh = S R2 R1  (upper tile products)
-  {
-    const int nup = nb * (nb + 1) / 2;
-    for (int task = cta; task < 3 * nup; task += C) {
-      const int kind = task / nup;
-      int I, J;
-      upper_pair(task % nup, 0, nb, I, J);
-      double acc[2][2];
-      if (kind == 0) {
-        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
-          const int K = I + q;
-          A = TRef{tile_ptr(a.US, bp, I, K), bp, 0};
-          B = TRef{tile_ptr(a.Li, bp, J, K), bp, 1};
-        }, s);
-        acc_each(acc, [&](int r, int c, double v) {
-          const int gr = I * TS + r, gc = J * TS + c;
-          if (gr < b && gc < b) {
-            a.Tw[gr + gc * a.ldt] = (gr <= gc) ? v : 0.0;
-            if (gr == gc) a.tau[gr] = v;
-          }
-        });
-      } else if (kind == 1) {
-        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
-          const int K = I + q;
-          A = TRef{tile_ptr(a.R2i, bp, I, K), bp, 0};
-          B = TRef{tile_ptr(a.Ui, bp, K, J), bp, 0};
-        }, s);
-        acc_to_global(acc, tile_ptr(a.M, bp, I, J), bp, 1.0);
-      } else {
-        tile_sum(acc, J - I + 1, [&](int q, TRef& A, TRef& B) {
-          const int K = I + q;
-          A = TRef{tile_ptr(a.R2, bp, I, K), bp, 0};
-          B = TRef{tile_ptr(a.R1, bp, K, J), bp, 0};
-        }, s);
-        acc_each(acc, [&](int r, int c, double v) {
-          const int gr = I * TS + r, gc = J * TS + c;
-          if (gr < b && gc < b) a.Rh[gr + gc * a.ldr] = (gr <= gc) ? __ldcg(a.S + gr) * v : 0.0;
-        });
-      }
-      __syncthreads();
-    }
-    // strictly-lower tiles of the outputs
-    for (int task = cta; task < nb * nb; task += C) {
-      const int I = task % nb, J = task / nb;
-      if (I <= J) continue;
-      for (int e = threadIdx.x; e < TS * TS; e += SNT) {
-        const int gr = I * TS + (e & 31), gc = J * TS + (e >> 5);
-        if (gr < b && gc < b) {
-          a.Tw[gr + gc * a.ldt] = 0.0;
-          a.Rh[gr + gc * a.ldr] = 0.0;
-        }
-      }
-    }
-  }
+  cl.sync();
   if (cta == 0 && threadIdx.x == 0) {
     const bool bad1 = a.stats1[0] != 0.0;
     *a.flag = (bad1 || s.bad) ? 1 : 0;
+  }
+}
+
+// kernel 2b: sign-modified LU of F (padded bp x bp, F = -Q(0:b,:) R2^-1) with
+// L^-1, U~^-1 built along; then US = U~ S.  Zeroes the tiles of Li above and
+// of Ui / US below the diagonal first.
+__global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm_raw[];
+  SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
+  const SmallDims d = a.d;
+  const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+  const int bp = d.bp;
+  const int64_t tot = int64_t(bp) * bp;
+  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+    const int r = int(e % bp), c = int(e / bp);
+    if (r / TS > c / TS) {
+      a.Ui[e] = 0.0;
+      a.US[e] = 0.0;
+    }
+    if (r / TS < c / TS) a.Li[e] = 0.0;
+  }
+  cluster_barrier(cl);
+  lu_sign_inv_dev(cl, d, a.F, a.Li, a.Ui, a.S, s);
+  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
+    const int r = int(e % bp), c = int(e / bp);
+    if (r / TS <= c / TS) a.US[e] = (r <= c) ? __ldcg(a.F + e) * __ldcg(a.S + c) : 0.0;
+  }
+}
+
+// kernel 2c (any grid): tau = diag(T_w), R_h = S (R2 R1) (upper), zeros below
+// the diagonal of R_h and T_w.
+__global__ void recon_finish_k(int b, int bp, const double* __restrict__ S, const double* __restrict__ RR,
+                               double* __restrict__ Rh, int64_t ldr, double* __restrict__ Tw, int64_t ldt,
+                               double* __restrict__ tau) {
+  const int64_t tot = int64_t(b) * b;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(e % b), c = int(e / b);
+    Rh[r + c * ldr] = (r <= c) ? S[r] * RR[r + int64_t(c) * bp] : 0.0;
+    if (r > c) Tw[r + c * ldt] = 0.0;
+    if (r == c) tau[r] = Tw[r + c * ldt];
   }
 }
 
@@ -689,11 +739,16 @@ __global__ void put_unit_lower_k(int b, const double* __restrict__ F, int bp, do
 
 template <class K, class... Args>
 void launch_cluster(K kern, cudaStream_t st, int C, Args... args) {
-  static bool attr = false;
+  // one attribute call per kernel (several kernels share the type K)
+  static std::mutex mu;
+  static std::vector<const void*> done;
   const size_t smem = sizeof(SmallSm);
-  if (!attr) {
-    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), (const void*)kern) == done.end()) {
+      RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      done.push_back((const void*)kern);
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
@@ -748,7 +803,7 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w) {
 }
 
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
-                 int64_t ldr, double* tau, double* Tw, int64_t ldt) {
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems) {
   ReconArgs a;
   a.d = SmallDims{(int)b, w.bp, w.bp / TS};
   a.W2 = w.W2;
@@ -771,9 +826,29 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
   a.tau = tau;
   a.flag = w.flag;
   a.dev_max = 0.5;
-  ProfScope _p(st, C_QR_SMALL, 0.0);
-  count_launch(C_QR_SMALL);
-  launch_cluster(recon_k, st, SC, a);
+  const int bp = w.bp;
+  {
+    ProfScope _p(st, C_QR_SMALL, 0.0);
+    count_launch(C_QR_SMALL);
+    launch_cluster(recon_r2_k, st, SC, a);
+  }
+  // the b x b products run GPU-wide (upper-triangular right operands: TRMM)
+  dgemm(st, false, false, b, b, b, -1.0, Q1, ldq, w.R2i, bp, 0.0, w.F, bp, part, part_elems, 0, true);  // F
+  {
+    ProfScope _p(st, C_QR_SMALL, 0.0);
+    count_launch(C_QR_SMALL);
+    launch_cluster(recon_lu_k, st, SC, a);
+  }
+  dgemm(st, false, true, b, b, b, 1.0, w.US, bp, w.Li, bp, 0.0, Tw, ldt, part, part_elems, 0, true);   // T = US Li^T
+  dgemm(st, false, false, b, b, b, 1.0, w.R2i, bp, w.Ui, bp, 0.0, w.M, bp, part, part_elems, 0, true);  // M = R2^-1 U~^-1
+  dgemm(st, false, false, b, b, b, 1.0, w.R2, bp, w.R1, bp, 0.0, w.US, bp, part, part_elems, 0, true);  // R2 R1
+  {
+    ProfScope _p(st, C_QR_SMALL, 0.0);
+    count_launch(C_QR_SMALL);
+    recon_finish_k<<<(int)std::min<int64_t>(cdiv(b * b, 256), 256), 256, 0, st>>>((int)b, bp, w.S, w.US, R, ldr, Tw,
+                                                                                    ldt, tau);
+    RUTV_LAUNCH_CK();
+  }
 }
 
 void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv) {

@@ -1,7 +1,7 @@
 // Phase timing of the b x b cluster kernels (smallmat.cu) with %globaltimer
 // stamps from CTA 0 / thread 0: build with
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/small_prof \
-//        tools/small_prof.cu paper_1703_00998_b200/csrc/prof.cu
+//        tools/small_prof.cu paper_1703_00998_b200/csrc/{prof,gemm,misc}.cu
 // and run on the GPU: prints, per block step, the ns spent in each phase.
 #include <cstdio>
 #include <vector>
@@ -43,7 +43,18 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    rutv::small_chol_inv(0, b, w);
+    if (argc > 2) {  // LU of a diagonally dominant F (recon_lu_k)
+      std::vector<double> F(bp * bp, 0.0);
+      for (int i = 0; i < b; ++i)
+        for (int j = 0; j < b; ++j) F[i + j * bp] = (i == j ? 3.0 : 0.0) + ((rand() / (double)RAND_MAX) - 0.5) / b;
+      cudaMemcpy(w.F, F.data(), F.size() * 8, cudaMemcpyHostToDevice);
+      rutv::ReconArgs a{};
+      a.d = rutv::SmallDims{b, (int)bp, (int)bp / 32};
+      a.F = w.F; a.Li = w.Li; a.Ui = w.Ui; a.US = w.US; a.S = w.S;
+      rutv::launch_cluster(rutv::recon_lu_k, 0, rutv::SC, a);
+    } else {
+      rutv::small_chol_inv(0, b, w);
+    }
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
