@@ -47,7 +47,7 @@ const std::vector<double>& prof_timeline();
 // b_upper: op(B) is upper triangular (only k <= j contributes to column j; TRMM).
 void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* part,
-           size_t part_elems, int force_splits = 0, bool b_upper = false);
+           size_t part_elems, int force_splits = 0, bool b_upper = false, bool c_upper = false);
 // op(A) op(B) with the K range split: partial products at part + z*M*N (ld M),
 // z < returned split count; no reduction (the caller sums in fixed order).
 int dgemm_partials(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,

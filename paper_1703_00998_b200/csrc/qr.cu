@@ -506,10 +506,10 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     GemmRole role(C_GEMM_QR);
     SmallWork sw = carve_small(w.small, b);
     const int bp = sw.bp;
-    dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems);        // G1
+    dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);  // G1 (upper)
     small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
     dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems, 0, true);  // Q1
-    dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems);      // G2
+    dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems, 0, false, true);  // G2
     const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
     small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems);
@@ -531,7 +531,7 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
     GemmRole role(C_GEMM_QR);
     SmallWork sw = carve_small(w.small, b);
     const int bp = sw.bp;
-    dgemm(st, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, bp, w.part, w.part_elems);
+    dgemm(st, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);
     small_chol_inv(st, b, sw);
     // kappa(R1) estimated by its diagonal: CholeskyQR's loss of orthogonality
     // ~ kappa^2 eps stays <= 1e-8 -- ample for a basis of the power loop

@@ -638,8 +638,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
     const int64_t tot = int64_t(bp) * bp;
     for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
       const int r = int(e % bp), c = int(e / bp);
-      if (r < b && c < b) {
-        const double v = a.W2[e] - (r == c ? 1.0 : 0.0);
+      if (r < b && c < b) {  // the upper triangle (the Gram GEMM writes only that)
+        const double v = (r <= c) ? a.W2[e] - (r == c ? 1.0 : 0.0) : 0.0;
         dev = fmax(dev, isfinite(v) ? fabs(v) : 1e300);
       } else {
         a.W2[e] = (r == c) ? 1.0 : 0.0;
