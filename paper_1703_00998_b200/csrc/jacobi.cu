@@ -369,7 +369,23 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
   double* B = Bw + int64_t(mat) * k * k;
   double* W = Wm + int64_t(mat) * k * k;
   // global <-> shared for one block (16 columns, zero padding beyond k)
+  // (16-byte accesses when k is even: a column pair of rows r, r+1 is aligned)
+  const bool vec = (k & 1) == 0;
   auto load_block = [&](int blk, int slot) {
+    if (vec) {
+      for (int idx = threadIdx.x; idx < KB * KP / 2; idx += JNT) {
+        const int c = idx / (KP / 2), r = 2 * (idx % (KP / 2)), g = blk * KB + c;
+        const bool ok = g < k && r < k;  // k even: r < k implies r + 1 < k
+        double2 vb = make_double2(0.0, 0.0), vw = vb;
+        if (ok) {
+          vb = __ldcg(reinterpret_cast<const double2*>(B + r + int64_t(g) * k));
+          vw = __ldcg(reinterpret_cast<const double2*>(W + r + int64_t(g) * k));
+        }
+        *reinterpret_cast<double2*>(sB + (slot * KB + c) * KP + r) = vb;
+        *reinterpret_cast<double2*>(sW + (slot * KB + c) * KP + r) = vw;
+      }
+      return;
+    }
     for (int idx = threadIdx.x; idx < KB * KP; idx += JNT) {
       const int c = idx / KP, r = idx % KP, g = blk * KB + c;
       const bool ok = g < k && r < k;
@@ -378,6 +394,18 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
     }
   };
   auto store_block = [&](int blk, int slot) {
+    if (vec) {
+      for (int idx = threadIdx.x; idx < KB * KP / 2; idx += JNT) {
+        const int c = idx / (KP / 2), r = 2 * (idx % (KP / 2)), g = blk * KB + c;
+        if (g < k && r < k) {
+          __stcg(reinterpret_cast<double2*>(B + r + int64_t(g) * k),
+                 *reinterpret_cast<const double2*>(sB + (slot * KB + c) * KP + r));
+          __stcg(reinterpret_cast<double2*>(W + r + int64_t(g) * k),
+                 *reinterpret_cast<const double2*>(sW + (slot * KB + c) * KP + r));
+        }
+      }
+      return;
+    }
     for (int idx = threadIdx.x; idx < KB * KP; idx += JNT) {
       const int c = idx / KP, r = idx % KP, g = blk * KB + c;
       if (g < k && r < k) {
@@ -420,7 +448,10 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
           __syncthreads();
         }
       }
-      // cross pairs: warp w holds column w of block p
+      // cross pairs: warp w holds column w of block p and meets column
+      // (w + sh) mod 16 of block q in sub-round sh.  (A per-column flag
+      // handoff between neighbouring warps instead of the barrier was
+      // measured: no faster.)
       JacCol<EPL> xb, xw;
       jc_lds(xb, sB + warp * KP, lane);
       jc_lds(xw, sW + warp * KP, lane);

@@ -278,25 +278,27 @@ __device__ __noinline__ void cta_chol_inv(SmallSm& s, int gcol0, int b) {
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) A[i * LD + j0 + jj] = a[jj];
   __syncthreads();
-  if (tid < TS) {
+  if (tid < TS) {  // warp 0: pivots, their reciprocals, breakdown flag, min / max
     double p = A[tid * LD + tid];
     const bool ok = (p > 0.0) && isfinite(p);
     if (!ok) p = 1.0;
     const double d = sqrt(p);
     s.piv[tid] = d;
-    s.c[tid] = 1.0 / d;
-    if (gcol0 + tid < b && !ok) atomicOr(&s.bad, 1);
+    s.c[tid] = frcp(d);
+    const bool valid = gcol0 + tid < b;
+    if (valid && !ok) atomicOr(&s.bad, 1);
+    double mn = valid ? d : DBL_MAX, mx = valid ? d : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) {
+      s.dmin = fmin(s.dmin, mn);
+      s.dmax = fmax(s.dmax, mx);
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    double mn = s.dmin, mx = s.dmax;
-    for (int k = 0; k < TS && gcol0 + k < b; ++k) {
-      mn = fmin(mn, s.piv[k]);
-      mx = fmax(mx, s.piv[k]);
-    }
-    s.dmin = mn;
-    s.dmax = mx;
-  }
   const double* rd = s.c;
   for (int e = tid; e < TS * TS; e += SNT) {
     const int i = e & 31, j = e >> 5;  // (row i, col j), column-major outputs
@@ -380,7 +382,7 @@ __device__ __noinline__ void cta_lu_sign_inv(SmallSm& s) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) A[i * LD + 32 * r + 4 * g + q] = a[4 * r + q];
   __syncthreads();
-  if (tid < TS) s.c[tid] = 1.0 / s.piv[tid];
+  if (tid < TS) s.c[tid] = frcp(s.piv[tid]);
   __syncthreads();
   const double* rp = s.c;
   for (int e = tid; e < TS * TS; e += SNT) {
