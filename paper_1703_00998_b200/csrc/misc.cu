@@ -54,17 +54,16 @@ __global__ void ident_k(int64_t m, int64_t n, double* D, int64_t ldd, double dia
 __global__ void norm_partial_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds,
                                double* __restrict__ D, int64_t ldd, double* partials, int* flag) {
   __shared__ double red[TB / 32];
-  const int64_t total = m * n;
   double acc = 0.0;
   int bad = 0;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    int64_t i = idx % m, j = idx / m;
-    double v = S[i + j * lds];
-    if (D) D[i + j * ldd] = v;
-    if (!isfinite(v)) bad = 1;
-    acc = fma(v, v, acc);
-  }
+  // column-strided (fixed partition: deterministic; no 64-bit division per element)
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x)
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      double v = S[i + j * lds];
+      if (D) D[i + j * ldd] = v;
+      if (!isfinite(v)) bad = 1;
+      acc = fma(v, v, acc);
+    }
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   if (bad && flag) atomicOr(flag, 1);
@@ -76,12 +75,19 @@ __global__ void norm_partial_k(int64_t m, int64_t n, const double* __restrict__ 
   }
 }
 
+// fixed-order (deterministic) sum of the partials: strided per thread, then a
+// shared-memory tree (one 256-thread block)
 __global__ void norm_final_k(int nparts, const double* partials, double* out2) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < nparts; ++i) s += partials[i];
-    out2[0] = s;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) s += partials[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out2[0] = red[0];
 }
 
 __global__ void gaussian_k(double* G, int64_t ldg, int64_t rows, int64_t cols, uint32_t k0, uint32_t k1,
@@ -144,10 +150,10 @@ void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
 
 void copy_norm_check(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D,
                      int64_t ldd, double* scratch, double* out2, int* flag) {
-  int blocks = std::min(grid_for(m * n), 4096);
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n, 4096));
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag); }
   RUTV_LAUNCH_CK();
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 256, 0, st>>>(blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 
@@ -156,10 +162,10 @@ void fro2(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, d
     RUTV_CK(cudaMemsetAsync(out2, 0, sizeof(double), st));
     return;
   }
-  int blocks = std::min(grid_for(m * n), 4096);
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n, 4096));
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, nullptr, 0, scratch, nullptr); }
   RUTV_LAUNCH_CK();
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 32, 0, st>>>(blocks, scratch, out2); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 256, 0, st>>>(blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 

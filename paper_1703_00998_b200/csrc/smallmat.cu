@@ -574,9 +574,8 @@ __device__ void init_stats(SmallSm& s) {
 __device__ void init_gram_and_zero(cg::cluster_group& cl, const SmallDims& d, double* W, double* const* zl, int nzl) {
   const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
   const int bp = d.bp, b = d.b;
-  const int64_t tot = int64_t(bp) * bp;
-  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-    const int r = int(e % bp), c = int(e / bp);
+  for (int c = cta; c < bp; c += C)  // column-strided: no 64-bit division per element
+    for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
     if (r >= b || c >= b) W[e] = (r == c) ? 1.0 : 0.0;
     const int ti = r / TS, tj = c / TS;
     if (ti > tj)
@@ -637,9 +636,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
   // ---- deviation of G2 from I (before padding), padding, zero lower tiles
   {
     double dev = 0.0;
-    const int64_t tot = int64_t(bp) * bp;
-    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-      const int r = int(e % bp), c = int(e / bp);
+    for (int c = cta; c < bp; c += C)
+      for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
       if (r < b && c < b) {  // the upper triangle (the Gram GEMM writes only that)
         const double v = (r <= c) ? a.W2[e] - (r == c ? 1.0 : 0.0) : 0.0;
         dev = fmax(dev, isfinite(v) ? fabs(v) : 1e300);
@@ -671,9 +669,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
   // (R2^T R2 = I + U + U^T + O(E^2) = I + E), so the 8-step Cholesky is skipped.
   const double devmax = __longlong_as_double((long long)*cl.map_shared_rank(&s.devbits, 0));
   if (double(b) * devmax <= 1e-8) {
-    const int64_t tot = int64_t(bp) * bp;
-    for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-      const int r = int(e % bp), c = int(e / bp);
+    for (int c = cta; c < bp; c += C)
+      for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
       const double ev = (r < b && c < b) ? a.W2[e] - (r == c ? 1.0 : 0.0) : 0.0;
       const double u = (r < c) ? ev : (r == c ? 0.5 * ev : 0.0);
       a.R2[e] = (r == c ? 1.0 : 0.0) + u;
@@ -699,9 +696,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
   const SmallDims d = a.d;
   const int C = (int)cl.num_blocks(), cta = (int)cl.block_rank();
   const int bp = d.bp;
-  const int64_t tot = int64_t(bp) * bp;
-  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-    const int r = int(e % bp), c = int(e / bp);
+  for (int c = cta; c < bp; c += C)  // column-strided: no 64-bit division per element
+    for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
     if (r / TS > c / TS) {
       a.Ui[e] = 0.0;
       a.US[e] = 0.0;
@@ -710,8 +706,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
   }
   cluster_barrier(cl);
   lu_sign_inv_dev(cl, d, a.F, a.Li, a.Ui, a.S, s);
-  for (int64_t e = int64_t(cta) * SNT + threadIdx.x; e < tot; e += int64_t(C) * SNT) {
-    const int r = int(e % bp), c = int(e / bp);
+  for (int c = cta; c < bp; c += C)  // column-strided: no 64-bit division per element
+    for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
     if (r / TS <= c / TS) a.US[e] = (r <= c) ? __ldcg(a.F + e) * __ldcg(a.S + c) : 0.0;
   }
 }
@@ -721,9 +717,8 @@ __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
 __global__ void recon_finish_k(int b, int bp, const double* __restrict__ S, const double* __restrict__ RR,
                                double* __restrict__ Rh, int64_t ldr, double* __restrict__ Tw, int64_t ldt,
                                double* __restrict__ tau) {
-  const int64_t tot = int64_t(b) * b;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
-    const int r = int(e % b), c = int(e / b);
+  for (int c = blockIdx.x; c < b; c += gridDim.x)
+    for (int r = threadIdx.x; r < b; r += blockDim.x) {
     Rh[r + c * ldr] = (r <= c) ? S[r] * RR[r + int64_t(c) * bp] : 0.0;
     if (r > c) Tw[r + c * ldt] = 0.0;
     if (r == c) tau[r] = Tw[r + c * ldt];
@@ -732,9 +727,8 @@ __global__ void recon_finish_k(int b, int bp, const double* __restrict__ S, cons
 
 // V(0:b, 0:b) <- unit lower L (strict lower part of F, ld bp)
 __global__ void put_unit_lower_k(int b, const double* __restrict__ F, int bp, double* __restrict__ V, int64_t ldv) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(b) * b;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int r = int(e % b), c = int(e / b);
+  for (int c = blockIdx.x; c < b; c += gridDim.x)
+    for (int r = threadIdx.x; r < b; r += blockDim.x) {
     V[r + c * ldv] = (r > c) ? F[r + int64_t(c) * bp] : (r == c ? 1.0 : 0.0);
   }
 }
@@ -847,7 +841,7 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
   {
     ProfScope _p(st, C_QR_SMALL, 0.0);
     count_launch(C_QR_SMALL);
-    recon_finish_k<<<(int)std::min<int64_t>(cdiv(b * b, 256), 256), 256, 0, st>>>((int)b, bp, w.S, w.US, R, ldr, Tw,
+    recon_finish_k<<<(int)std::min<int64_t>(b, 256), 256, 0, st>>>((int)b, bp, w.S, w.US, R, ldr, Tw,
                                                                                     ldt, tau);
     RUTV_LAUNCH_CK();
   }
