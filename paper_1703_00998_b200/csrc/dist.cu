@@ -385,6 +385,8 @@ class DistFactor {
   ~DistFactor() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_fork2_) cudaEventDestroy(ev_fork2_);
+    if (ev_join2_) cudaEventDestroy(ev_join2_);
   }
 
  private:
@@ -402,6 +404,7 @@ class DistFactor {
   double a_fro_ = 0.0;
   bool opt_ = false;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;  // owner's right-apply overlap
+  cudaEvent_t ev_fork2_ = nullptr, ev_join2_ = nullptr;  // owner's panel QR on the priority stream
   std::vector<int> nflags_;  // per local rank: optimistic flag slots used
   // number of steps si < s with si = r (mod P), i.e. the slot of the next owned step
   int64_t own_slot(int64_t s, int r) const { return blocks_before(s, r, P); }
@@ -499,6 +502,20 @@ cudaStream_t dist_side_stream() {
   return streams[dev];
 }
 
+// highest-priority stream for the owner's panel QR (see driver.cu priority_stream)
+cudaStream_t dist_priority_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, greatest));
+  }
+  return streams[dev];
+}
+
 // low-priority side stream for the owner's trailing right-apply update
 cudaStream_t dist_update_stream() {
   static cudaStream_t streams[64] = {};
@@ -522,6 +539,8 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   fallbacks = 0;
   if (!ev_fork_) RUTV_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   if (!ev_join_) RUTV_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  if (!ev_fork2_) RUTV_CK(cudaEventCreateWithFlags(&ev_fork2_, cudaEventDisableTiming));
+  if (!ev_join2_) RUTV_CK(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
 
   // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
   for (auto& lr : L) {
@@ -749,9 +768,14 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       for (size_t l = 0; l < L.size(); ++l) {
         auto& lr = L[l];
         if (lr.r != owner) continue;
+        // the owner's panel QR runs on the highest-priority stream so that its
+        // GEMMs are not queued behind the side-stream update's CTAs
+        cudaStream_t hp = dist_priority_stream();
+        RUTV_CK(cudaEventRecord(ev_fork2_, st));
+        RUTV_CK(cudaStreamWaitEvent(hp, ev_fork2_, 0));
         double* X = lr.T + r0 + c0[l] * lr.ldt;
         double* Wu = lr.w.pack;
-        copy_matrix(st, mi, b, X, lr.ldt, Wu, mi);
+        copy_matrix(hp, mi, b, X, lr.ldt, Wu, mi);
         QrWork qw = lr.w.qw;
         qw.mode = o.qr_mode;
         qw.fallbacks = &fallbacks;
@@ -760,11 +784,13 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           qw.flag_count = &nflags_[l];
           qw.flag_cap = lr.w.qflags_cap;
         }
-        int rc = panel_qr(st, mi, b, Wu, mi, Wu + wun + size_t(b) * b, b, lr.w.tau, Wu + wun, b, qw);
+        int rc = panel_qr(hp, mi, b, Wu, mi, Wu + wun + size_t(b) * b, b, lr.w.tau, Wu + wun, b, qw);
         if (rc != OK) return rc;
         // T(I2,J2) = R11 (replaced by D after the SVD), T(I3,J2) = 0
-        copy_matrix(st, b, b, Wu + wun + size_t(b) * b, b, X, lr.ldt);
-        set_zero(st, mi - b, b, X + b, lr.ldt);
+        copy_matrix(hp, b, b, Wu + wun + size_t(b) * b, b, X, lr.ldt);
+        set_zero(hp, mi - b, b, X + b, lr.ldt);
+        RUTV_CK(cudaEventRecord(ev_join2_, hp));
+        RUTV_CK(cudaStreamWaitEvent(st, ev_join2_, 0));
       }
       comm.bcast(bufs(&RankWork::pack), wun + 2 * size_t(b) * b, owner, st);
       for (auto& lr : L) {  // keep R11 for the deferred SVD (and W_u, T_u for U)
