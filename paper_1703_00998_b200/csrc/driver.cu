@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -171,9 +172,9 @@ void dg(const Work& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, 
 // Low-priority side stream per device for work off the critical path (the
 // deferred b x b SVDs): its kernels fill the SMs the latency-bound panel-QR
 // kernels leave idle, and the block scheduler prefers the main stream's CTAs.
-// which = 0: deferred SVD chunks; 1: trailing right-apply updates.
+// which = 0: deferred SVD chunks; 1: trailing right-apply updates; 2: D2H copies of final T blocks.
 cudaStream_t side_stream(int which = 0) {
-  static cudaStream_t streams[2][64] = {};
+  static cudaStream_t streams[3][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return nullptr;
@@ -220,9 +221,12 @@ int check_qr(int rc) {
 // The factorization proper (device pointers only).
 constexpr int kRetry = 1000;  // factor_device: an optimistic CholeskyQR decision failed, redo synchronously
 
+// on_final(c): enqueued work on the factorization's stream has made columns
+// 0..c-1 of T final (used to overlap the D2H of host-staged calls).
 int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
                   uint64_t seed, int64_t k_stop, double* U, double* T, double* V, randutv_info* info,
-                  void* ws, size_t ws_bytes, bool optimistic) {
+                  void* ws, size_t ws_bytes, bool optimistic,
+                  const std::function<void(int64_t)>& on_final = std::function<void(int64_t)>()) {
   cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
   const bool uv = (U != nullptr);
   const bool reortho = (o.no_reortho == 0);
@@ -283,6 +287,33 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     RUTV_CK(cudaEventRecord(done, side));
     chunks.push_back({s0, steps, done});
     svd_done = steps;
+  };
+  // ---- folds into T, one SVD chunk at a time on the main stream
+  // once that chunk's SVDs are done: T(I2,J2) = D, T(I2,J3) = Us^T T(I2,J3),
+  // T(I1,J2) = T(I1,J2) Vs.  They act on rows above / columns left of the
+  // trailing matrix and commute with the later steps' one-sided transforms
+  // (left vs right products), so a chunk is folded inside the loop one chunk
+  // after its SVDs were launched; afterwards the column blocks of its steps
+  // are final.
+  size_t folded = 0;
+  auto fold_chunk = [&](const SvdChunk& ch) {
+    if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
+    set_gemm_role(C_GEMM_OTHER);
+    for (int64_t si = ch.s0; si < ch.s1; ++si) {
+      const int64_t r0 = b * si;
+      const double* Us = w.Usall + size_t(si) * b * b;
+      const double* Vs = w.Vsall + size_t(si) * b * b;
+      write_diag_block(st, b, b, w.Dall + si * b, T + r0 + r0 * m, m);            // T(I2,J2) = D
+      const int64_t nc = n - r0 - b;
+      if (nc > 0) {                                                                // T(I2,J3) = Us^T T(I2,J3)
+        dg(w, st, true, false, b, nc, b, 1.0, Us, b, T + r0 + (r0 + b) * m, m, 0.0, w.fold, b);
+        copy_matrix(st, b, nc, w.fold, b, T + r0 + (r0 + b) * m, m);
+      }
+      if (r0 > 0) {                                                                // T(I1,J2) = T(I1,J2) Vs
+        dg(w, st, false, false, r0, b, b, 1.0, T + r0 * m, m, Vs, b, 0.0, w.fold, r0);
+        copy_matrix(st, r0, b, w.fold, r0, T + r0 * m, m);
+      }
+    }
   };
   int64_t r0f = 0, nif = 0, mif = 0;
   double trailing = 0.0;
@@ -381,7 +412,14 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       dg(w, st, false, true, mi, nc, b, -1.0, Wu, ldwu, w.Wt2, n, 1.0, Cm, m);      // C -= W_u (.)^T
       ++steps;
       k_done = f2;
-      if (svd_side && steps - svd_done >= kSvdChunk) launch_svd_chunk();
+      if (svd_side && steps - svd_done >= kSvdChunk) {
+        if (folded < chunks.size()) {  // the previous chunk (launched kSvdChunk steps ago)
+          fold_chunk(chunks[folded]);
+          if (on_final) on_final(b * chunks[folded].s1);
+          ++folded;
+        }
+        launch_svd_chunk();
+      }
       if (o.tol > 0.0) {
         double t2 = 0.0;
         fro2(st, m - e2, n - f2, T + e2 + f2 * m, m, w.nrm, w.scal);
@@ -441,27 +479,8 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   if (final_block)
     jacobi_svd_batched(st, 1, (int)kf, w.Rfin, kf, kf * kf, w.Dfin, w.Usfin, w.Vsfin, w.jworkf, w.sweeps + steps);
 
-  // ---- folds into T (deferred), chunk by chunk as the side-stream
-  // SVDs complete (all folds stay on the main stream: left and right products
-  // commute, so their order does not matter, but they must not run concurrently)
-  for (const SvdChunk& ch : chunks) {
-    if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
-  for (int64_t si = ch.s0; si < ch.s1; ++si) {
-    const int64_t r0 = b * si;
-    const double* Us = w.Usall + size_t(si) * b * b;
-    const double* Vs = w.Vsall + size_t(si) * b * b;
-    write_diag_block(st, b, b, w.Dall + si * b, T + r0 + r0 * m, m);            // T(I2,J2) = D
-    const int64_t nc = n - r0 - b;
-    if (nc > 0) {                                                                // T(I2,J3) = Us^T T(I2,J3)
-      dg(w, st, true, false, b, nc, b, 1.0, Us, b, T + r0 + (r0 + b) * m, m, 0.0, w.fold, b);
-      copy_matrix(st, b, nc, w.fold, b, T + r0 + (r0 + b) * m, m);
-    }
-    if (r0 > 0) {                                                                // T(I1,J2) = T(I1,J2) Vs
-      dg(w, st, false, false, r0, b, b, 1.0, T + r0 * m, m, Vs, b, 0.0, w.fold, r0);
-      copy_matrix(st, r0, b, w.fold, r0, T + r0 * m, m);
-    }
-  }
-  }
+  // ---- the remaining folds (the last chunks)
+  for (; folded < chunks.size(); ++folded) fold_chunk(chunks[folded]);
   for (cudaEvent_t e : evs) cudaEventDestroy(e);
   if (final_block && final_fat) {
     // T(I2, J) = [diag(D) 0];  T(I1, J) <- T(I1, J) Q blockdiag(Ur, I)
@@ -703,20 +722,49 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     double* dV = U ? dU + size_t(m) * m : nullptr;
     RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
                               cudaMemcpyDefault, st));
-    rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, true);
+    // T host buffer pinned: copy T's column blocks back as they become final
+    // (after each in-loop fold) on a copy stream, overlapping the rest of the
+    // factorization; the remainder is copied at the end
+    int64_t copied = 0;
+    cudaStream_t cps = nullptr;
+    cudaEvent_t cev = nullptr;
+    std::function<void(int64_t)> on_final;
+    cudaPointerAttributes tat;
+    if (!U && cudaPointerGetAttributes(&tat, T) == cudaSuccess && tat.type == cudaMemoryTypeHost) {
+      cps = side_stream(2);
+      RUTV_CK(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming));
+      on_final = [&](int64_t cols) {
+        cols = std::min(cols, n);
+        if (cols <= copied) return;
+        RUTV_CK(cudaEventRecord(cev, st));
+        RUTV_CK(cudaStreamWaitEvent(cps, cev, 0));
+        RUTV_CK(cudaMemcpyAsync(T + size_t(copied) * m, dT + size_t(copied) * m, sizeof(double) * m * (cols - copied),
+                                cudaMemcpyDeviceToHost, cps));
+        copied = cols;
+      };
+    } else {
+      cudaGetLastError();
+    }
+    rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, true, on_final);
     if (rc == kRetry) {  // the input was factored in place: stage it again
+      if (cps) RUTV_CK(cudaStreamSynchronize(cps));  // in-flight copies of the discarded run
+      copied = 0;
       RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
                                 cudaMemcpyDefault, st));
-      rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, false);
+      rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, false, on_final);
     }
     if (rc == RANDUTV_OK) {
-      RUTV_CK(cudaMemcpyAsync(T, dT, sizeof(double) * m * n, cudaMemcpyDefault, st));
+      if (copied < n)
+        RUTV_CK(cudaMemcpyAsync(T + size_t(copied) * m, dT + size_t(copied) * m, sizeof(double) * m * (n - copied),
+                                cudaMemcpyDefault, st));
       if (U) {
         RUTV_CK(cudaMemcpyAsync(U, dU, sizeof(double) * m * m, cudaMemcpyDefault, st));
         RUTV_CK(cudaMemcpyAsync(V, dV, sizeof(double) * n * n, cudaMemcpyDefault, st));
       }
     }
     RUTV_CK(cudaStreamSynchronize(st));
+    if (cps) RUTV_CK(cudaStreamSynchronize(cps));
+    if (cev) cudaEventDestroy(cev);
     return rc;
   } catch (const CudaError& e) {
     fprintf(stderr, "randutv: CUDA error %s at %s\n", cudaGetErrorString(e.e), e.where);

@@ -245,6 +245,21 @@ def test_host_buffers_match_device():
     assert np.array_equal(Th, to_host(T)) and np.array_equal(Uh, to_host(U))
 
 
+def test_pinned_host_buffers_overlapped_copy_back():
+    """T-only on PINNED host buffers: T's column blocks are copied back while
+    the factorization runs (after each in-loop fold); the result must be the
+    device path's bits.  23 steps = several SVD chunks, so several copies."""
+    A = testmat.gaussian(1500, 1500, 21)
+    b, q, seed = 64, 1, 3
+    m, n = A.shape
+    Ah = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory()   # (n, m) row-major = A column-major
+    Th = torch.empty(n, m, dtype=torch.float64).pin_memory()
+    rc = P.factor_raw(m, n, Ah.data_ptr(), m, b, q, seed, 0, None, Th.data_ptr(), None)
+    assert rc == 0
+    _, T, _, _ = P.randutv(to_dev(A), b, q, seed, with_uv=False)
+    assert torch.equal(Th.t(), T.cpu())
+
+
 def test_deterministic():
     c = testmat.config("c2", scale=0.1)
     _, T1, _, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed, with_uv=False)
