@@ -260,7 +260,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   bool final_block = false, final_tall = false, final_fat = false;
   // The b x b SVDs of R11 are independent of later steps (R13): with
   // the single-cluster Jacobi kernel they run in chunks on the side stream.
-  constexpr int64_t kSvdChunk = 8;
+  constexpr int64_t kSvdChunk = 8;  // measured at c3: 4 / 8 / 12 / 16 / all-at-end = 274.8 / 272.2 / 272.6 / 275.6 / 278.0 ms
   const bool svd_side = jacobi_single_launch((int)b);
   cudaStream_t side = svd_side ? side_stream() : nullptr;
   int64_t svd_done = 0;
@@ -292,9 +292,9 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // once that chunk's SVDs are done: T(I2,J2) = D, T(I2,J3) = Us^T T(I2,J3),
   // T(I1,J2) = T(I1,J2) Vs.  They act on rows above / columns left of the
   // trailing matrix and commute with the later steps' one-sided transforms
-  // (left vs right products), so a chunk is folded inside the loop one chunk
-  // after its SVDs were launched; afterwards the column blocks of its steps
-  // are final.
+  // (left vs right products), so a chunk may be folded inside the loop one
+  // chunk after its SVDs were launched; afterwards the column blocks of its
+  // steps are final.
   size_t folded = 0;
   auto fold_chunk = [&](const SvdChunk& ch) {
     if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
@@ -413,7 +413,11 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       ++steps;
       k_done = f2;
       if (svd_side && steps - svd_done >= kSvdChunk) {
-        if (folded < chunks.size()) {  // the previous chunk (launched kSvdChunk steps ago)
+        // host-staged calls only: folding inside the loop puts the folds on the
+        // critical path (+2 ms at c3) but lets T's final blocks stream back to
+        // the host during the loop (-7 ms); device calls fold at the end, where
+        // the folds hide behind the last SVD chunk
+        if (on_final && folded < chunks.size()) {  // the previous chunk (launched kSvdChunk steps ago)
           fold_chunk(chunks[folded]);
           if (on_final) on_final(b * chunks[folded].s1);
           ++folded;

@@ -246,9 +246,11 @@ def test_host_buffers_match_device():
 
 
 def test_pinned_host_buffers_overlapped_copy_back():
-    """T-only on PINNED host buffers: T's column blocks are copied back while
-    the factorization runs (after each in-loop fold); the result must be the
-    device path's bits.  23 steps = several SVD chunks, so several copies."""
+    """T-only on PINNED host buffers: the folds of each SVD chunk are applied
+    inside the loop and T's finished column blocks are copied back while the
+    factorization runs (23 steps = several chunks, several copies).  The device
+    path folds at the end, so the two agree to rounding (left and right
+    products applied in a different order), with identical exact zeros."""
     A = testmat.gaussian(1500, 1500, 21)
     b, q, seed = 64, 1, 3
     m, n = A.shape
@@ -257,7 +259,12 @@ def test_pinned_host_buffers_overlapped_copy_back():
     rc = P.factor_raw(m, n, Ah.data_ptr(), m, b, q, seed, 0, None, Th.data_ptr(), None)
     assert rc == 0
     _, T, _, _ = P.randutv(to_dev(A), b, q, seed, with_uv=False)
-    assert torch.equal(Th.t(), T.cpu())
+    Th, T = Th.t().numpy(), to_host(T)
+    assert np.array_equal(Th == 0.0, T == 0.0)
+    assert np.abs(Th - T).max() <= 1e-12 * np.linalg.norm(A)
+    ref = oracle.randutv(A, b, q, seed, build_ortho=False)
+    par = check_parity(Th, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
 
 
 def test_deterministic():
