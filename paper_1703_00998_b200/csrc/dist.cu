@@ -1189,6 +1189,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
     const size_t per = rutv::dist_rank_bytes(d);
     char* ws = (char*)rutv::dist_ws(per * nlr);
     if (!ws) return RANDUTV_ERR_NOMEM;
+    rutv::poison_workspace(ws, per * nlr, o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread);
     std::vector<rutv::LocalRank> L(nlr);
     for (int l = 0; l < nlr; ++l) {
       auto& lr = L[l];

@@ -611,6 +611,11 @@ void* cached_ws(size_t bytes) {
     }
     g_ws_bytes = bytes;
   }
+  if (getenv("RANDUTV_POISON_WORKSPACE")) {  // test hook, see poison_workspace (misc.cu)
+    RUTV_CK(cudaDeviceSynchronize());
+    RUTV_CK(cudaMemset(g_ws, 0xFF, g_ws_bytes));
+    RUTV_CK(cudaDeviceSynchronize());
+  }
   return g_ws;
 }
 
@@ -702,6 +707,7 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     } else if (wsb < need) {
       return -12;
     }
+    poison_workspace(ws, wsb, st);
     // Optimistic first (no host synchronisation per panel QR); the synchronous
     // per-panel fallback run only if a CholeskyQR decision failed.  Not when T
     // aliases A (the first run would have destroyed the input).

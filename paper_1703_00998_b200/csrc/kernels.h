@@ -45,6 +45,7 @@ const std::vector<double>& prof_timeline();
 // C = alpha op(A) op(B) + beta C.  ``part`` (part_elems doubles) is the split-K
 // scratch; force_splits > 0 overrides the split heuristic.
 // b_upper: op(B) is upper triangular (only k <= j contributes to column j; TRMM).
+void poison_workspace(void* p, size_t bytes, cudaStream_t st);  // test hook (driver.cu)
 void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* part,
            size_t part_elems, int force_splits = 0, bool b_upper = false, bool c_upper = false);

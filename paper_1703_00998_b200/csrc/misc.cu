@@ -2,6 +2,8 @@
 // non-finite scan (input validation), the Philox Gaussian draw.
 #include "common.cuh"
 #include "kernels.h"
+
+#include <cstdlib>
 #include "philox.cuh"
 
 #include <algorithm>
@@ -182,6 +184,14 @@ void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, do
   if (m <= 0 || k <= 0) return;
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); diag_block_k<<<grid2(m, k), TB, 0, st>>>(m, k, d, D, ldd); }
   RUTV_LAUNCH_CK();
+}
+
+// Test hook (an initcheck substitute: compute-sanitizer is not available on
+// the GPU pool): RANDUTV_POISON_WORKSPACE=1 fills the workspace with NaN bit
+// patterns before each factorization, so a read of workspace memory that was
+// never written shows up as NaN in the results.
+void poison_workspace(void* p, size_t bytes, cudaStream_t st) {
+  if (p && bytes && getenv("RANDUTV_POISON_WORKSPACE")) RUTV_CK(cudaMemsetAsync(p, 0xFF, bytes, st));
 }
 
 }  // namespace rutv

@@ -13,6 +13,7 @@ import oracle  # noqa: E402
 import paper_1703_00998_b200 as P  # noqa: E402
 import testmat  # noqa: E402
 from util import EPS, check_parity, diag_blocks_ok, ek_fro, invariants  # noqa: E402
+from paper_1703_00998_b200 import dist as D_  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -351,3 +352,38 @@ def test_rsvd_vs_oracle(m, n, b, q, p, decay):
     assert abs(e_gpu - e_orc) <= 1e-8 * e_orc + floor
     assert np.linalg.norm(U.T @ U - np.eye(b)) < 1e-13 * m and np.linalg.norm(V.T @ V - np.eye(b)) < 1e-13 * n
     assert np.all(np.diff(D) <= 0)
+
+
+def test_poisoned_workspace_initcheck():
+    """compute-sanitizer is closed on the GPU pool; instead every workspace is
+    filled with NaN bit patterns before use (RANDUTV_POISON_WORKSPACE), so a
+    kernel reading workspace memory it never wrote would put NaN into the
+    results.  Outputs must be finite and equal to the normal run."""
+    import os
+    c = testmat.config("c1")
+    A2 = testmat.gaussian(700, 520, 9)
+    runs = []
+    for poison in (False, True):
+        if poison:
+            os.environ["RANDUTV_POISON_WORKSPACE"] = "1"
+        try:
+            out = []
+            U, T, V, _ = P.randutv(to_dev(c.A), c.b, c.q, c.seed)
+            out += [U, T, V]
+            _, T2, _, _ = P.randutv(to_dev(A2), 64, 2, 4, with_uv=False, oversample=6)
+            _, T3, _, _ = P.randutv(to_dev(A2), 64, 1, 4, with_uv=False, qr_mode=1)
+            out += [T2, T3]
+            Uk, D, Vk = P.rsvd(to_dev(A2), 48, 1, 5)
+            out += [Uk, D, Vk]
+            comm = D_.loopback(3)
+            sh = [D_.shard(to_dev(A2), 64, r, 3) for r in range(3)]
+            Us, Ts, Vs, _ = D_.factor(comm, sh, 700, 520, 64, 1, 2, with_uv=True)
+            comm.close()
+            out += [D_.assemble(Us, 700, 64), D_.assemble(Ts, 520, 64), D_.assemble(Vs, 520, 64)]
+            torch.cuda.synchronize()
+            runs.append([to_host(x) for x in out])
+        finally:
+            os.environ.pop("RANDUTV_POISON_WORKSPACE", None)
+    for a, p in zip(*runs):
+        assert np.all(np.isfinite(p))
+        assert np.array_equal(a, p)
