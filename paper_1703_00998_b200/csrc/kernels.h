@@ -91,8 +91,11 @@ SmallWork carve_small(double* base, int64_t b);
 void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w);
 // W2 = Q1^T Q1 -> second pass + Householder reconstruction: writes R (b x b,
 // ld ldr), tau, Tw (ld ldt), w.M = R2^-1 U~^-1 and w.F (L strictly below), w.flag.
+// side (optional): T_w, tau and R_h are formed on it (forked after the LU with
+// ev_fork); the caller must wait for ev_join before using them.
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
-                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems);
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems,
+                 cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr);
 // V(0:b, 0:b) <- unit lower L from w.F
 void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv);
 

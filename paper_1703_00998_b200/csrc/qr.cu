@@ -498,6 +498,27 @@ bool cholqr_ok(const QrWork& w, int64_t m, int64_t b) {
 // the panel and two cluster kernels -- with the column-by-column Householder
 // kernel as the fallback when the panel is too ill-conditioned for CholeskyQR2
 // (Cholesky breakdown or ||Q1^T Q1 - I||_max > 1/2, i.e. kappa >~ 1e7).
+// highest-priority helper stream (per device) for the reconstruction's
+// T_w / R_h products, and its fork / join events
+cudaStream_t recon_side_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, greatest));
+  }
+  return streams[dev];
+}
+cudaEvent_t recon_event(int which) {
+  static cudaEvent_t evs[2][64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
+  return evs[which][dev];
+}
+
 int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
              double* Tw, int64_t ldt, const QrWork& w) {
   if (b <= 0) return OK;
@@ -512,14 +533,18 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems, 0, false, true);  // G2
     const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
-    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems);
-    if (optimistic || read_flag_sync(st, sw.flag) == 0) {
+    cudaStream_t rs = recon_side_stream();
+    cudaEvent_t ef = recon_event(0), ej = recon_event(1);
+    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems, rs, ef, ej);
+    const bool ok = optimistic || read_flag_sync(st, sw.flag) == 0;
+    if (ok) {
       if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
         dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems, 0,
               true);
       small_put_unit_lower(st, b, sw, V, ldv);
-      return OK;
     }
+    RUTV_CK(cudaStreamWaitEvent(st, ej, 0));  // T_w, tau, R_h
+    if (ok) return OK;
     if (w.fallbacks) ++*w.fallbacks;
   }
   return panel_qr_hh(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);

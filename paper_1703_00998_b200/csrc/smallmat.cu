@@ -799,7 +799,8 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w) {
 }
 
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
-                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems) {
+                 int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems,
+                 cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
   ReconArgs a;
   a.d = SmallDims{(int)b, w.bp, w.bp / TS};
   a.W2 = w.W2;
@@ -835,16 +836,27 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
     count_launch(C_QR_SMALL);
     launch_cluster(recon_lu_k, st, SC, a);
   }
-  dgemm(st, false, true, b, b, b, 1.0, w.US, bp, w.Li, bp, 0.0, Tw, ldt, part, part_elems, 0, true);   // T = US Li^T
+  // M (needed next by W = -Q1(b:) M) stays on st; T_w, tau and R_h are not
+  // needed until after the caller's W GEMM, so with a side stream they are
+  // formed concurrently with it (unsplit GEMMs: the split-K scratch is st's)
+  cudaStream_t ts = side ? side : st;
+  if (side) {
+    RUTV_CK(cudaEventRecord(ev_fork, st));
+    RUTV_CK(cudaStreamWaitEvent(side, ev_fork, 0));
+  }
+  double* tpart = side ? nullptr : part;
+  const size_t tpe = side ? 0 : part_elems;
   dgemm(st, false, false, b, b, b, 1.0, w.R2i, bp, w.Ui, bp, 0.0, w.M, bp, part, part_elems, 0, true);  // M = R2^-1 U~^-1
-  dgemm(st, false, false, b, b, b, 1.0, w.R2, bp, w.R1, bp, 0.0, w.US, bp, part, part_elems, 0, true);  // R2 R1
+  dgemm(ts, false, true, b, b, b, 1.0, w.US, bp, w.Li, bp, 0.0, Tw, ldt, tpart, tpe, 0, true);     // T = US Li^T
+  dgemm(ts, false, false, b, b, b, 1.0, w.R2, bp, w.R1, bp, 0.0, w.W2, bp, tpart, tpe, 0, true);   // R2 R1 (W2 is free)
   {
-    ProfScope _p(st, C_QR_SMALL, 0.0);
+    ProfScope _p(ts, C_QR_SMALL, 0.0);
     count_launch(C_QR_SMALL);
-    recon_finish_k<<<(int)std::min<int64_t>(b, 256), 256, 0, st>>>((int)b, bp, w.S, w.US, R, ldr, Tw,
+    recon_finish_k<<<(int)std::min<int64_t>(b, 256), 256, 0, ts>>>((int)b, bp, w.S, w.W2, R, ldr, Tw,
                                                                                     ldt, tau);
     RUTV_LAUNCH_CK();
   }
+  if (side) RUTV_CK(cudaEventRecord(ev_join, side));
 }
 
 void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv) {
