@@ -32,6 +32,8 @@ using namespace rutv;
 
 namespace {
 
+constexpr int kYFlags = 16;  // per-step sketch-side CholeskyQR decision slots (reorthos, QR(Y))
+
 std::mutex g_mu;
 void* g_ws = nullptr;
 size_t g_ws_bytes = 0;
@@ -139,8 +141,10 @@ Work carve(Arena& ar, const Plan& p) {
   w.scal = ar.take<double>(16);
   w.flag = ar.take<int>(16);
   w.sweeps = ar.take<int>(size_t(sb) + 16);
-  w.qflags_cap = int((p.q + 2) * std::max<int64_t>(p.nrand, 1) + 8);
-  w.qflags = ar.take<int>(size_t(w.qflags_cap));
+  // panel-QR decisions (one per step + final block) and, after them, one
+  // step's sketch-side decisions (reorthos, over-sampling QR, QR(Y))
+  w.qflags_cap = int(std::max<int64_t>(p.nrand, 1) + 8);
+  w.qflags = ar.take<int>(size_t(w.qflags_cap) + kYFlags);
   return w;
 }
 
@@ -206,7 +210,7 @@ cudaStream_t priority_stream() {
 }
 
 cudaEvent_t overlap_event(int which) {
-  static cudaEvent_t evs[4][64] = {};
+  static cudaEvent_t evs[5][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
@@ -244,6 +248,20 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     w.qw.flag_count = &nflags;
     w.qw.flag_cap = w.qflags_cap;
   }
+  // The re-orthonormalisations and QR(Y) of a step touch no part of T, so
+  // their CholeskyQR decisions are checked per step: the step's device flags
+  // are copied to the host right after QR(Y), ahead of the P = T W_v GEMM, and
+  // read while that GEMM runs; if one failed (rank-deficient sketches: c5 step
+  // 4), only this step's sketch and QR(Y) are redone with synchronous decisions
+  // (Householder fallback in place) -- no whole-factorization retry.  The
+  // column panel QR stays optimistic (flags checked once after the loop).
+  QrWork qw_sync = w.qw;
+  qw_sync.dev_flags = nullptr;
+  qw_sync.flag_count = nullptr;
+  const bool opt_y = optimistic && o.qr_mode == 0;
+  static int* h_yflags = nullptr;  // pinned host copy of one step's flags
+  if (opt_y && !h_yflags) RUTV_CK(cudaMallocHost(&h_yflags, sizeof(int) * kYFlags));
+  cudaEvent_t ev_yflags = overlap_event(4);
 
   // ---- T <- A, ||A||_F, non-finite scan (one host sync)
   RUTV_CK(cudaMemsetAsync(w.flag, 0, sizeof(int), st));
@@ -327,48 +345,73 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     double* X = T + r0 + r0 * m;
     if (b * i < m && b * i < n) {
       const int64_t si = i - 1;  // 0-based step slot
-      // ---- sketch
-      set_gemm_role(C_GEMM_SKETCH);
-      const int64_t p_i = std::min<int64_t>(p.ovs, ni - b);  // over-sampling (R23); 0 = Fig. fig:randUTV
-      const int64_t bw = b + p_i;                            // sketch width
-      gaussian_fill(st, w.G, m, mi, bw, seed, uint32_t(i - 1), 0u);
-      dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
-      double* Ycur = w.Y;
-      double* Yalt = w.Y2;
-      for (int it = 0; it < q; ++it) {
-        if (reortho) {
-          check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, w.qw));
+      double* Wv = nullptr;
+      int64_t ldwv = n;
+      double* Tv = w.Tv + size_t(si) * b * b;
+      double* TJ = T + r0 * m;
+      // sketch, QR(Y) and P = T W_v, P2 = P T_v: reads T only
+      auto sketch_qr_p = [&](const QrWork& qwy, bool copy_flags) {
+        // ---- sketch
+        set_gemm_role(C_GEMM_SKETCH);
+        const int64_t p_i = std::min<int64_t>(p.ovs, ni - b);  // over-sampling (R23); 0 = Fig. fig:randUTV
+        const int64_t bw = b + p_i;                            // sketch width
+        gaussian_fill(st, w.G, m, mi, bw, seed, uint32_t(i - 1), 0u);
+        dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
+        double* Ycur = w.Y;
+        double* Yalt = w.Y2;
+        for (int it = 0; it < q; ++it) {
+          if (reortho) {
+            check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, qwy));
+            std::swap(Ycur, Yalt);
+          }
+          dg(w, st, false, false, mi, bw, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);      // Z = X Y
+          dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);       // Y = X^T Z
+        }
+        if (p_i > 0) {
+          // Y <- the b dominant left singular vectors of the extended Y (P:1133-1135,
+          // Fig. fig:stepUTVoversampling ``[Z,~,~] = svd(Y,'econ')``): Y = Q R,
+          // R = Us D Vs^T, Z = Q Us(:, 1:b).  Column signs of Z are free (R9/A.3).
+          GemmRole role(C_GEMM_QR);
+          check_qr(panel_qr(st, ni, bw, Ycur, n, w.Ro, bw, w.tau, w.Ttmp, bw, qwy));
+          thin_q(st, ni, bw, Ycur, n, w.Ttmp, bw, w.Qo, n, w.Rtmp, w.part, w.part_elems);
+          jacobi_svd_batched(st, 1, (int)bw, w.Ro, bw, bw * bw, w.Do, w.Uso, w.Vso, w.jworko, nullptr);
+          dg(w, st, false, false, ni, b, bw, 1.0, w.Qo, n, w.Uso, bw, 0.0, Yalt, n);
           std::swap(Ycur, Yalt);
         }
-        dg(w, st, false, false, mi, bw, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);      // Z = X Y
-        dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);       // Y = X^T Z
+        // ---- V block: Householder QR of Y
+        Wv = Ycur;
+        ldwv = n;
+        if (uv) {
+          Wv = w.Wv_all + p.off_v[si];
+          ldwv = ni;
+          copy_matrix(st, ni, b, Ycur, n, Wv, ldwv);
+        }
+        check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
+        if (copy_flags && *qwy.flag_count > 0) {
+          RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
+          RUTV_CK(cudaEventRecord(ev_yflags, st));
+        }
+        // ---- right apply to all m rows: P = T W_v, P2 = P T_v
+        set_gemm_role(C_GEMM_RIGHT);
+        dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
+        dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
+      };
+      if (opt_y) {
+        int ny = 0;
+        QrWork qwy = w.qw;
+        qwy.dev_flags = w.qflags + w.qflags_cap;  // the kYFlags slots after the panel-QR ones
+        qwy.flag_count = &ny;
+        qwy.flag_cap = kYFlags;
+        sketch_qr_p(qwy, true);
+        bool failed = false;
+        if (ny > 0) {  // read while the P GEMM runs
+          RUTV_CK(cudaEventSynchronize(ev_yflags));
+          for (int f = 0; f < ny; ++f) failed |= h_yflags[f] != 0;
+        }
+        if (failed) sketch_qr_p(qw_sync, false);
+      } else {
+        sketch_qr_p(qw_sync, false);
       }
-      if (p_i > 0) {
-        // Y <- the b dominant left singular vectors of the extended Y (P:1133-1135,
-        // Fig. fig:stepUTVoversampling ``[Z,~,~] = svd(Y,'econ')``): Y = Q R,
-        // R = Us D Vs^T, Z = Q Us(:, 1:b).  Column signs of Z are free (R9/A.3).
-        GemmRole role(C_GEMM_QR);
-        check_qr(panel_qr(st, ni, bw, Ycur, n, w.Ro, bw, w.tau, w.Ttmp, bw, w.qw));
-        thin_q(st, ni, bw, Ycur, n, w.Ttmp, bw, w.Qo, n, w.Rtmp, w.part, w.part_elems);
-        jacobi_svd_batched(st, 1, (int)bw, w.Ro, bw, bw * bw, w.Do, w.Uso, w.Vso, w.jworko, nullptr);
-        dg(w, st, false, false, ni, b, bw, 1.0, w.Qo, n, w.Uso, bw, 0.0, Yalt, n);
-        std::swap(Ycur, Yalt);
-      }
-      // ---- V block: Householder QR of Y
-      double* Wv = Ycur;
-      int64_t ldwv = n;
-      if (uv) {
-        Wv = w.Wv_all + p.off_v[si];
-        ldwv = ni;
-        copy_matrix(st, ni, b, Ycur, n, Wv, ldwv);
-      }
-      double* Tv = w.Tv + size_t(si) * b * b;
-      check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, w.qw));
-      // ---- right apply to all m rows
-      set_gemm_role(C_GEMM_RIGHT);
-      double* TJ = T + r0 * m;
-      dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
-      dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
       // The panel QR below reads only the panel block T(r0:m, J2): update it
       // first on the main stream; the rest of the rank-b update (columns J3 and
       // the rows above the panel) runs on a low-priority side stream
@@ -463,6 +506,10 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     std::vector<int> hf(nflags);
     RUTV_CK(cudaMemcpyAsync(hf.data(), w.qflags, sizeof(int) * nflags, cudaMemcpyDeviceToHost, st));
     RUTV_CK(cudaStreamSynchronize(st));
+    if (getenv("RANDUTV_DEBUG_FLAGS")) {  // diagnostics only
+      for (int i = 0; i < nflags; ++i)
+        if (hf[i]) fprintf(stderr, "randutv: CholeskyQR decision %d of %d failed\n", i, nflags);
+    }
     for (int f : hf)
       if (f) {
         if (svd_side) RUTV_CK(cudaStreamSynchronize(side));
