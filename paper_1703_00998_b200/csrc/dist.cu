@@ -219,6 +219,8 @@ inline int grid_for_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int
 // ----------------------------------------------------------------------------- the distributed driver
 namespace {
 
+constexpr int kDistYFlags = 16;  // per-step sketch-side CholeskyQR decision slots (reorthos, QR(Y))
+
 struct RankWork {
   // shapes: m rows; nl = local columns
   double *G, *Y, *Y2, *Z, *P, *P2, *S, *S2, *pack, *q1, *small, *part, *fold;
@@ -296,8 +298,8 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   }
   w.flag = ar.take<int>(16);
   w.sweeps = ar.take<int>(size_t(sb) + 16);
-  w.qflags_cap = int(16 * sb + 16);  // reortho + QR(Y) + panel-QR decisions
-  w.qflags = ar.take<int>(size_t(w.qflags_cap));
+  w.qflags_cap = int(16 * sb + 16);  // panel-QR decisions
+  w.qflags = ar.take<int>(size_t(w.qflags_cap) + kDistYFlags);  // + one step's sketch-side decisions
   w.qw.part = w.part;
   w.qw.part_elems = w.part_elems;
   w.qw.sfull = ar.take<double>(size_t(32) * b);
@@ -387,6 +389,8 @@ class DistFactor {
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_fork2_) cudaEventDestroy(ev_fork2_);
     if (ev_join2_) cudaEventDestroy(ev_join2_);
+    if (ev_yflags_) cudaEventDestroy(ev_yflags_);
+    if (h_yflags_) cudaFreeHost(h_yflags_);
   }
 
  private:
@@ -405,13 +409,11 @@ class DistFactor {
   bool opt_ = false;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;  // owner's right-apply overlap
   cudaEvent_t ev_fork2_ = nullptr, ev_join2_ = nullptr;  // owner's panel QR on the priority stream
+  cudaEvent_t ev_yflags_ = nullptr;  // the step's sketch-side decision flags are on the host
+  int* h_yflags_ = nullptr;          // pinned
   std::vector<int> nflags_;  // per local rank: optimistic flag slots used
   // number of steps si < s with si = r (mod P), i.e. the slot of the next owned step
   int64_t own_slot(int64_t s, int r) const { return blocks_before(s, r, P); }
-  int* next_flag(size_t l) {
-    auto& w = L[l].w;
-    return (nflags_[l] < w.qflags_cap) ? w.qflags + nflags_[l]++ : nullptr;
-  }
   std::vector<double*> bufs(double* RankWork::*member) {
     std::vector<double*> v;
     for (auto& lr : L) v.push_back(lr.w.*member);
@@ -541,6 +543,8 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   if (!ev_join_) RUTV_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   if (!ev_fork2_) RUTV_CK(cudaEventCreateWithFlags(&ev_fork2_, cudaEventDisableTiming));
   if (!ev_join2_) RUTV_CK(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
+  if (!ev_yflags_) RUTV_CK(cudaEventCreateWithFlags(&ev_yflags_, cudaEventDisableTiming));
+  if (!h_yflags_) RUTV_CK(cudaMallocHost(&h_yflags_, sizeof(int) * kDistYFlags));
 
   // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
   for (auto& lr : L) {
@@ -632,110 +636,135 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     }
     if (b * i < m && b * i < n) {
       const int64_t si = p;
-      // ---- sketch
-      set_gemm_role(C_GEMM_SKETCH);
-      for (size_t l = 0; l < L.size(); ++l) {
-        auto& lr = L[l];
-        gaussian_fill(st, lr.w.G, m, mi, b, seed, uint32_t(p), 0u);
-        dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.G, m, 0.0, lr.w.Y,
-           std::max<int64_t>(nt[l], 1));
-      }
-      for (int it = 0; it < q; ++it) {
-        if (reortho) {
-          set_gemm_role(C_GEMM_QR);
-          dist_gram_chol(&RankWork::Y, nt, 1);
-          bool ok;
-          if (opt_) {  // decision flags on the device, checked once after the loop
-            for (size_t l = 0; l < L.size(); ++l) {
-              int* f = next_flag(l);
-              if (f) reortho_flag(st, L[l].sw.stats, 1e4, f);
-            }
-            ok = true;
-          } else {
-            double h[3];
-            RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-            RUTV_CK(cudaStreamSynchronize(st));
-            ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
-          }
-          if (ok) {
-            for (size_t l = 0; l < L.size(); ++l) {
-              auto& lr = L[l];
-              dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
-                 lr.w.Y2, std::max<int64_t>(nt[l], 1), true);
-            }
-          } else {
-            int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr);
-            if (rc != OK) return rc;
-          }
-          for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
-          set_gemm_role(C_GEMM_SKETCH);
-        }
-        for (size_t l = 0; l < L.size(); ++l) {  // Z = X Y  (partial)
-          auto& lr = L[l];
-          dg(lr.w, st, false, false, mi, b, nt[l], 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
-             std::max<int64_t>(nt[l], 1), 0.0, lr.w.Z, mi);
-        }
-        comm.allreduce(bufs(&RankWork::Z), size_t(mi) * b, st);
-        for (size_t l = 0; l < L.size(); ++l) {  // Y = X^T Z
-          auto& lr = L[l];
-          dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Z, mi, 0.0,
-             lr.w.Y, std::max<int64_t>(nt[l], 1));
-        }
-      }
-      // ---- QR(Y) -> W_v (rows distributed), T_v
-      set_gemm_role(C_GEMM_QR);
+      // Sketch, QR(Y) and the partial P = T W_v touch no part of T: the sketch
+      // side's CholeskyQR decisions are read per step while the P GEMM runs,
+      // and a failure redoes only this step's part with synchronous decisions
+      // (Householder fallback) on every rank alike.
       std::vector<double*> Tv(L.size());
-      for (size_t l = 0; l < L.size(); ++l) Tv[l] = L[l].w.Tfin;  // T_v of this step
-      bool qr_ok = false;
-      if (o.qr_mode == 0) {
-        dist_gram_chol(&RankWork::Y, nt, 1);
+      int lam_err = OK;
+      auto sketch_qr_p = [&](bool opt_y) -> int {
+        int ny = 0;
+        // ---- sketch
+        set_gemm_role(C_GEMM_SKETCH);
         for (size_t l = 0; l < L.size(); ++l) {
           auto& lr = L[l];
-          dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
-             lr.w.q1, std::max<int64_t>(nt[l], 1), true);
+          gaussian_fill(st, lr.w.G, m, mi, b, seed, uint32_t(p), 0u);
+          dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.G, m, 0.0, lr.w.Y,
+             std::max<int64_t>(nt[l], 1));
         }
-        dist_gram_chol(&RankWork::q1, nt, 2);
-        // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
-        for (size_t l = 0; l < L.size(); ++l) {
-          auto& lr = L[l];
-          if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, std::max<int64_t>(nt[l], 1), lr.w.pack, b);
+        for (int it = 0; it < q; ++it) {
+          if (reortho) {
+            set_gemm_role(C_GEMM_QR);
+            dist_gram_chol(&RankWork::Y, nt, 1);
+            bool ok;
+            if (opt_y && ny < kDistYFlags) {  // decision flags on the device, read after QR(Y)
+              for (size_t l = 0; l < L.size(); ++l)
+                reortho_flag(st, L[l].sw.stats, 1e4, L[l].w.qflags + L[l].w.qflags_cap + ny);
+              ++ny;
+              ok = true;
+            } else {
+              double h[3];
+              RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+              RUTV_CK(cudaStreamSynchronize(st));
+              ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
+            }
+            if (ok) {
+              for (size_t l = 0; l < L.size(); ++l) {
+                auto& lr = L[l];
+                dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
+                   lr.w.Y2, std::max<int64_t>(nt[l], 1), true);
+              }
+            } else {
+              int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr);
+              if (rc != OK) { lam_err = rc; return -1; }
+            }
+            for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
+            set_gemm_role(C_GEMM_SKETCH);
+          }
+          for (size_t l = 0; l < L.size(); ++l) {  // Z = X Y  (partial)
+            auto& lr = L[l];
+            dg(lr.w, st, false, false, mi, b, nt[l], 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
+               std::max<int64_t>(nt[l], 1), 0.0, lr.w.Z, mi);
+          }
+          comm.allreduce(bufs(&RankWork::Z), size_t(mi) * b, st);
+          for (size_t l = 0; l < L.size(); ++l) {  // Y = X^T Z
+            auto& lr = L[l];
+            dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Z, mi, 0.0,
+               lr.w.Y, std::max<int64_t>(nt[l], 1));
+          }
         }
-        comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
-        for (size_t l = 0; l < L.size(); ++l) {
-          auto& lr = L[l];
-          SmallWork sw = lr.sw;
-          int* f = opt_ ? next_flag(l) : nullptr;
-          if (f) sw.flag = f;
-          small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b, lr.w.part, lr.w.part_elems);
-        }
-        qr_ok = opt_ ? true : (read_int_sync(st, L[0].sw.flag) == 0);
-        if (qr_ok) {
+        // ---- QR(Y) -> W_v (rows distributed), T_v
+        set_gemm_role(C_GEMM_QR);
+        for (size_t l = 0; l < L.size(); ++l) Tv[l] = L[l].w.Tfin;  // T_v of this step
+        bool qr_ok = false;
+        if (o.qr_mode == 0) {
+          dist_gram_chol(&RankWork::Y, nt, 1);
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
-            if (nt[l] > 0)
-              dg(lr.w, st, false, false, nt[l], b, b, -1.0, lr.w.q1, nt[l], lr.sw.M, bp, 0.0, lr.w.Y, nt[l], true);
-            if (lr.r == owner) small_put_unit_lower(st, b, lr.sw, lr.w.Y, std::max<int64_t>(nt[l], 1));
+            dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
+               lr.w.q1, std::max<int64_t>(nt[l], 1), true);
+          }
+          dist_gram_chol(&RankWork::q1, nt, 2);
+          // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
+          for (size_t l = 0; l < L.size(); ++l) {
+            auto& lr = L[l];
+            if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, std::max<int64_t>(nt[l], 1), lr.w.pack, b);
+          }
+          comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
+          for (size_t l = 0; l < L.size(); ++l) {
+            auto& lr = L[l];
+            SmallWork sw = lr.sw;
+            if (opt_y && ny < kDistYFlags) sw.flag = lr.w.qflags + lr.w.qflags_cap + ny;
+            small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b, lr.w.part, lr.w.part_elems);
+          }
+          const bool qr_flagged = opt_y && ny < kDistYFlags;
+          if (qr_flagged) ++ny;
+          qr_ok = qr_flagged ? true : (read_int_sync(st, L[0].sw.flag) == 0);
+          if (qr_ok) {
+            for (size_t l = 0; l < L.size(); ++l) {
+              auto& lr = L[l];
+              if (nt[l] > 0)
+                dg(lr.w, st, false, false, nt[l], b, b, -1.0, lr.w.q1, nt[l], lr.sw.M, bp, 0.0, lr.w.Y, nt[l], true);
+              if (lr.r == owner) small_put_unit_lower(st, b, lr.sw, lr.w.Y, std::max<int64_t>(nt[l], 1));
+            }
           }
         }
-      }
-      if (!qr_ok) {
-        int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 1, Tv.data());
-        if (rc != OK) return rc;
-        for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
-      }
-      if (plan_.uv)  // keep this rank's rows of W_v and T_v for the V formation
+        if (!qr_ok) {
+          int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 1, Tv.data());
+          if (rc != OK) { lam_err = rc; return -1; }
+          for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
+        }
+        if (plan_.uv)  // keep this rank's rows of W_v and T_v for the V formation
+          for (size_t l = 0; l < L.size(); ++l) {
+            auto& lr = L[l];
+            const int64_t ldy = std::max<int64_t>(nt[l], 1);
+            if (nt[l] > 0) copy_matrix(st, nt[l], b, lr.w.Y, ldy, lr.w.Wvl_all + plan_.off_vl[si], ldy);
+            copy_matrix(st, b, b, Tv[l], b, lr.w.Tv_all + size_t(si) * b * b, b);
+          }
+        // the step's sketch-side flags (identical on every rank: computed from
+        // allreduced Grams and the broadcast Q1 block) to the host, read while
+        // the P GEMM below runs
+        if (opt_y && ny > 0) {
+          RUTV_CK(cudaMemcpyAsync(h_yflags_, L[0].w.qflags + L[0].w.qflags_cap, sizeof(int) * ny,
+                                  cudaMemcpyDeviceToHost, st));
+          RUTV_CK(cudaEventRecord(ev_yflags_, st));
+        }
+        // ---- right apply to all m rows
+        set_gemm_role(C_GEMM_RIGHT);
         for (size_t l = 0; l < L.size(); ++l) {
           auto& lr = L[l];
-          const int64_t ldy = std::max<int64_t>(nt[l], 1);
-          if (nt[l] > 0) copy_matrix(st, nt[l], b, lr.w.Y, ldy, lr.w.Wvl_all + plan_.off_vl[si], ldy);
-          copy_matrix(st, b, b, Tv[l], b, lr.w.Tv_all + size_t(si) * b * b, b);
+          dg(lr.w, st, false, false, m, b, nt[l], 1.0, lr.T + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
+             std::max<int64_t>(nt[l], 1), 0.0, lr.w.P, m);
         }
-      // ---- right apply to all m rows
-      set_gemm_role(C_GEMM_RIGHT);
-      for (size_t l = 0; l < L.size(); ++l) {
-        auto& lr = L[l];
-        dg(lr.w, st, false, false, m, b, nt[l], 1.0, lr.T + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
-           std::max<int64_t>(nt[l], 1), 0.0, lr.w.P, m);
+        return opt_y ? ny : 0;
+      };
+      int ny = sketch_qr_p(opt_);
+      if (ny < 0) return lam_err;
+      if (ny > 0) {
+        RUTV_CK(cudaEventSynchronize(ev_yflags_));
+        bool failed = false;
+        for (int f = 0; f < ny; ++f) failed |= h_yflags_[f] != 0;
+        if (failed && sketch_qr_p(false) < 0) return lam_err;
       }
       comm.allreduce(bufs(&RankWork::P), size_t(m) * b, st);
       bool joined = false;
