@@ -43,7 +43,10 @@ namespace {
 constexpr int TS = 32;    // tile size
 constexpr int SLD = 36;   // smem tile stride (== 4 mod 16 doubles: conflict-free DMMA fragments)
 constexpr int SNT = 256;  // threads per CTA
-constexpr int SC = 8;     // CTAs per cluster
+#ifndef RUTV_SMALL_SC
+#define RUTV_SMALL_SC 8
+#endif
+constexpr int SC = RUTV_SMALL_SC;  // CTAs per cluster
 constexpr int TSZ = TS * SLD;
 
 struct SmallSm {
