@@ -520,7 +520,6 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
 
   set_gemm_role(C_GEMM_OTHER);
   // ---- batched small SVDs
-  int max_sweeps = 0;
   if (svd_side) {
     launch_svd_chunk();
   } else if (steps > 0) {

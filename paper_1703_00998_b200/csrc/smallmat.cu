@@ -69,9 +69,6 @@ struct TRef {
   int tr;           // op(X) = tr ? stored^T : stored
 };
 
-__device__ __forceinline__ const double* tile_ptr(const double* M, int ld, int i, int j) {
-  return M + i * TS + size_t(j) * TS * ld;
-}
 __device__ __forceinline__ double* tile_ptr(double* M, int ld, int i, int j) {
   return M + i * TS + size_t(j) * TS * ld;
 }
