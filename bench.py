@@ -159,19 +159,22 @@ def make_input(case_name, device, rank, scale=1.0):
 def run_reference(args):
     """--impl reference: the oracle (CPU) on the same config, bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import numpy as np
     import torch
     import testmat
     case_name = args.config
+    # the same workload as our arm at this N (weak scaling: n = 10000 N^(1/3))
+    scale = world ** (1.0 / 3.0) if (world > 1 and args.scaling == "weak") else 1.0
     if torch.cuda.is_available():
-        At, case = testmat.device_config(case_name, device="cuda")
+        At, case = testmat.device_config(case_name, device="cuda", scale=scale)
         A_host = np.asfortranarray(At.t().cpu().numpy())
         del At
         torch.cuda.empty_cache()
     else:
-        c = testmat.config(case_name)
+        c = testmat.config(case_name, scale=scale)
         A_host, case = c.A, c
     m, n = A_host.shape
     for _ in range(max(args.warmup, 0)):
@@ -186,7 +189,7 @@ def run_reference(args):
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(ts), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_desc(case, m, n),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
