@@ -210,7 +210,7 @@ cudaStream_t priority_stream() {
 }
 
 cudaEvent_t overlap_event(int which) {
-  static cudaEvent_t evs[5][64] = {};
+  static cudaEvent_t evs[6][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
@@ -288,6 +288,35 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     cudaEvent_t done;
   };
   std::vector<SvdChunk> chunks;
+  // With the incremental Jacobi (k <= 256) a chunk's SVDs advance one sweep
+  // at the start of each latency-bound QR chain of the following steps (the
+  // re-orthonormalisations and QR(Y), when most SMs are idle), and are
+  // finished when the next chunk starts; otherwise a chunk runs in one go.
+  const bool svd_incr = svd_side && jacobi_incremental((int)b);
+  struct ActiveChunk {
+    int64_t s0 = 0, s1 = 0;
+    bool on = false;
+  } active;
+  auto chunk_work = [&](int64_t s0) { return w.jwork + jacobi_work_elems((int)s0, (int)b); };
+  auto finish_active = [&]() {
+    if (!active.on) return;
+    const int64_t s0 = active.s0, cnt = active.s1 - active.s0;
+    jacobi_end(side, (int)cnt, (int)b, chunk_work(s0), w.Dall + s0 * b, w.Usall + size_t(s0) * b * b,
+               w.Vsall + size_t(s0) * b * b, w.sweeps + s0);
+    cudaEvent_t done;
+    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    evs.push_back(done);
+    RUTV_CK(cudaEventRecord(done, side));
+    chunks.push_back({s0, active.s1, done});
+    active.on = false;
+  };
+  auto svd_sweep_here = [&]() {  // one sweep of the active chunk, starting at this point of st
+    if (!active.on) return;
+    cudaEvent_t e = overlap_event(4 + 1);
+    RUTV_CK(cudaEventRecord(e, st));
+    RUTV_CK(cudaStreamWaitEvent(side, e, 0));
+    jacobi_sweeps(side, (int)(active.s1 - active.s0), (int)b, chunk_work(active.s0), 1);
+  };
   auto launch_svd_chunk = [&]() {
     if (steps <= svd_done) return;
     cudaEvent_t e;
@@ -296,17 +325,24 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     RUTV_CK(cudaEventRecord(e, st));
     RUTV_CK(cudaStreamWaitEvent(side, e, 0));
     const int64_t s0 = svd_done, cnt = steps - svd_done;
-    jacobi_svd_batched(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, w.Dall + s0 * b,
-                       w.Usall + size_t(s0) * b * b, w.Vsall + size_t(s0) * b * b,
-                       w.jwork + jacobi_work_elems((int)s0, (int)b), w.sweeps + s0);
-    cudaEvent_t done;
-    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    evs.push_back(done);
-    RUTV_CK(cudaEventRecord(done, side));
-    chunks.push_back({s0, steps, done});
+    if (svd_incr) {
+      finish_active();
+      jacobi_begin(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
+      active.s0 = s0;
+      active.s1 = steps;
+      active.on = true;
+    } else {
+      jacobi_svd_batched(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, w.Dall + s0 * b,
+                         w.Usall + size_t(s0) * b * b, w.Vsall + size_t(s0) * b * b, chunk_work(s0),
+                         w.sweeps + s0);
+      cudaEvent_t done;
+      RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      evs.push_back(done);
+      RUTV_CK(cudaEventRecord(done, side));
+      chunks.push_back({s0, steps, done});
+    }
     svd_done = steps;
-  };
-  // ---- folds into T, one SVD chunk at a time on the main stream
+  };  // ---- folds into T, one SVD chunk at a time on the main stream
   // once that chunk's SVDs are done: T(I2,J2) = D, T(I2,J3) = Us^T T(I2,J3),
   // T(I1,J2) = T(I1,J2) Vs.  They act on rows above / columns left of the
   // trailing matrix and commute with the later steps' one-sided transforms
@@ -361,6 +397,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         double* Yalt = w.Y2;
         for (int it = 0; it < q; ++it) {
           if (reortho) {
+            svd_sweep_here();
             check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, qwy));
             std::swap(Ycur, Yalt);
           }
@@ -386,6 +423,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
           ldwv = ni;
           copy_matrix(st, ni, b, Ycur, n, Wv, ldwv);
         }
+        svd_sweep_here();
         check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
         if (copy_flags && *qwy.flag_count > 0) {
           RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
@@ -460,7 +498,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         // critical path (+2 ms at c3) but lets T's final blocks stream back to
         // the host during the loop (-7 ms); device calls fold at the end, where
         // the folds hide behind the last SVD chunk
-        if (on_final && folded < chunks.size()) {  // the previous chunk (launched kSvdChunk steps ago)
+        if (on_final && folded < chunks.size()) {  // a chunk that ended at least one chunk ago
           fold_chunk(chunks[folded]);
           if (on_final) on_final(b * chunks[folded].s1);
           ++folded;
@@ -522,6 +560,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // ---- batched small SVDs
   if (svd_side) {
     launch_svd_chunk();
+    finish_active();
   } else if (steps > 0) {
     jacobi_svd_batched(st, (int)steps, (int)b, w.Rall, b, b * b, w.Dall, w.Usall, w.Vsall, w.jwork, w.sweeps);
     chunks.push_back({0, steps, nullptr});

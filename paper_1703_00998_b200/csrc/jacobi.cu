@@ -43,8 +43,10 @@ __global__ void jacobi_init_k(int batch, int k, const double* __restrict__ R, in
     B[idx] = Ri[c + int64_t(r) * ldr];  // B = R^T
     W[idx] = (r == c) ? 1.0 : 0.0;
   }
-  if (blockIdx.x == 0)
+  if (blockIdx.x == 0) {
     for (int s = threadIdx.x; s <= MAX_SWEEPS; s += blockDim.x) counts[mat * (MAX_SWEEPS + 1) + s] = (s == 0);
+    if (threadIdx.x == 0) counts[batch * (MAX_SWEEPS + 1) + mat] = 0;  // next sweep (-1: converged)
+  }
 }
 
 __device__ __forceinline__ void rr_pair(int nplayers, int round, int i, int& p, int& q) {
@@ -354,7 +356,7 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
 template <int EPL>
 __global__ void __launch_bounds__(JNT)
 jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts,
-                  double tol) {
+                  double tol, int max_sweeps) {
   constexpr int KB = 16, KP = 32 * EPL;  // block width, padded column length
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double js[];
@@ -414,7 +416,15 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
       }
     }
   };
-  for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+  // resumable: up to max_sweeps sweeps from the stored next-sweep index
+  // (counts[batch (MAX_SWEEPS + 1) + mat], -1 once a sweep made no rotation)
+  int* next = counts + int(gridDim.y) * (MAX_SWEEPS + 1) + mat;
+  const int s0 = __ldcg(next);
+  if (s0 < 0) return;
+  const int s1 = min(MAX_SWEEPS, s0 + max_sweeps);
+  int sweep = s0;
+  bool converged = false;
+  for (; sweep < s1; ++sweep) {
     if (threadIdx.x == 0) rot_sm = 0;
     int rot = 0;
     for (int round = 0; round < d.nb - 1; ++round) {
@@ -483,8 +493,13 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
     __threadfence();
     cluster.sync();
     const int total = atomicAdd(&cnt[sweep + 1], 0);
-    if (total == 0) break;
+    if (total == 0) {
+      converged = true;
+      break;
+    }
   }
+  cluster.sync();  // every CTA has read the next-sweep index
+  if (cta == 0 && threadIdx.x == 0) *next = (converged || sweep >= MAX_SWEEPS) ? -1 : sweep;
 }
 
 // sigma_j = ||B(:,j)||, sort descending, Us = W(:,perm), Vs = B(:,perm) / sigma.
@@ -611,6 +626,94 @@ bool jacobi_single_launch(int k) {
 
 size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 1); }
 
+namespace {
+// up to max_sweeps sweeps of jacobi_cluster2_k on every matrix of the batch
+void launch_c2(cudaStream_t st, int batch, int k, double* Bw, double* Wm, int* counts, int max_sweeps) {
+  JacobiDesc d = make_desc(k);
+  const int csize = d.nb / 2;
+  const double tol = double(k) * DBL_EPSILON;
+  const int epl = k <= 64 ? 2 : (k <= 128 ? 4 : 8);
+  const size_t smem2 = size_t(2) * 2 * 16 * 32 * epl * sizeof(double);
+  auto kern = epl == 2 ? jacobi_cluster2_k<2> : (epl == 4 ? jacobi_cluster2_k<4> : jacobi_cluster2_k<8>);
+  static bool attr2[3] = {false, false, false};
+  const int ai = epl == 2 ? 0 : (epl == 4 ? 1 : 2);
+  if (!attr2[ai]) {
+    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    attr2[ai] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize, batch, 1);
+  cfg.blockDim = dim3(JNT, 1, 1);
+  cfg.dynamicSmemBytes = smem2;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ProfScope _p(st, K_SVD, 0.0);
+  count_launch(K_SVD);
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, Bw, Wm, counts, tol, max_sweeps));
+}
+
+struct JacobiBufs {
+  double *Bw, *Wm;
+  int* counts;
+};
+JacobiBufs jacobi_bufs(double* work, int batch, int k) {
+  return {work, work + size_t(batch) * k * k, reinterpret_cast<int*>(work + size_t(2) * batch * k * k)};
+}
+void launch_init(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
+                 const JacobiBufs& jb) {
+  dim3 g((unsigned)std::min<int64_t>(cdiv(int64_t(k) * k, 256), 64), batch);
+  ProfScope _p(st, K_SVD, 0.0);
+  count_launch(K_SVD);
+  jacobi_init_k<<<g, 256, 0, st>>>(batch, k, R, ldr, strideR, jb.Bw, jb.Wm, jb.counts);
+  RUTV_LAUNCH_CK();
+}
+void launch_finalize(cudaStream_t st, int batch, int k, const JacobiBufs& jb, double* D, double* Us, double* Vs,
+                     int* sweeps_out);
+}  // namespace
+
+
+namespace {
+void launch_finalize(cudaStream_t st, int batch, int k, const JacobiBufs& jb, double* D, double* Us, double* Vs,
+                     int* sweeps_out) {
+  double* Bw = jb.Bw;
+  double* Wm = jb.Wm;
+  int* counts = jb.counts;
+  const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
+  static size_t attr_f = 0;
+  if (fsmem > 48 * 1024 && fsmem > attr_f) {
+    RUTV_CK(cudaFuncSetAttribute(jacobi_finalize_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+    attr_f = fsmem;
+  }
+  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out); }
+  RUTV_LAUNCH_CK();
+}
+}  // namespace
+
+bool jacobi_incremental(int k) { return k > 1 && k <= 256 && make_desc(k).kb == 16; }
+
+void jacobi_begin(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR, double* work) {
+  if (batch <= 0) return;
+  launch_init(st, batch, k, R, ldr, strideR, jacobi_bufs(work, batch, k));
+}
+void jacobi_sweeps(cudaStream_t st, int batch, int k, double* work, int nsweeps) {
+  if (batch <= 0) return;
+  JacobiBufs jb = jacobi_bufs(work, batch, k);
+  launch_c2(st, batch, k, jb.Bw, jb.Wm, jb.counts, nsweeps);
+}
+void jacobi_end(cudaStream_t st, int batch, int k, double* work, double* D, double* Us, double* Vs,
+                int* sweeps_out) {
+  if (batch <= 0) return;
+  JacobiBufs jb = jacobi_bufs(work, batch, k);
+  launch_c2(st, batch, k, jb.Bw, jb.Wm, jb.counts, MAX_SWEEPS);  // the remaining sweeps, if any
+  launch_finalize(st, batch, k, jb, D, Us, Vs, sweeps_out);
+}
+
 void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
                         double* D, double* Us, double* Vs, double* work, int* sweeps_out) {
   if (batch <= 0 || k <= 0) return;
@@ -626,31 +729,8 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
   const double tol = double(k) * DBL_EPSILON;
   const int csize = d.nb / 2;
-  if (k > 1 && k <= 256 && d.kb == 16) {
-    const int epl = k <= 64 ? 2 : (k <= 128 ? 4 : 8);
-    const size_t smem2 = size_t(2) * 2 * 16 * 32 * epl * sizeof(double);
-    auto kern = epl == 2 ? jacobi_cluster2_k<2> : (epl == 4 ? jacobi_cluster2_k<4> : jacobi_cluster2_k<8>);
-    static bool attr2[3] = {false, false, false};
-    const int ai = epl == 2 ? 0 : (epl == 4 ? 1 : 2);
-    if (!attr2[ai]) {
-      RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      attr2[ai] = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(csize, batch, 1);
-    cfg.blockDim = dim3(JNT, 1, 1);
-    cfg.dynamicSmemBytes = smem2;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = csize;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    ProfScope _p(st, K_SVD, 0.0);
-    count_launch(K_SVD);
-    RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, Bw, Wm, counts, tol));
+  if (jacobi_incremental(k)) {
+    launch_c2(st, batch, k, Bw, Wm, counts, MAX_SWEEPS);
   } else if (k > 1 && csize <= MAX_CLUSTER) {
 
     // one cluster per matrix runs every round and sweep in-kernel
@@ -703,14 +783,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
       chunk = 2;
     }
   }
-  const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
-  static size_t attr_f = 0;
-  if (fsmem > 48 * 1024 && fsmem > attr_f) {
-    RUTV_CK(cudaFuncSetAttribute(jacobi_finalize_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-    attr_f = fsmem;
-  }
-  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out); }
-  RUTV_LAUNCH_CK();
+  launch_finalize(st, batch, k, JacobiBufs{Bw, Wm, counts}, D, Us, Vs, sweeps_out);
 }
 
 }  // namespace rutv

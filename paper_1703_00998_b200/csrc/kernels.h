@@ -149,5 +149,13 @@ size_t jacobi_work_elems(int batch, int k);
 bool jacobi_single_launch(int k);
 void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
                         double* D, double* Us, double* Vs, double* work, int* sweeps_out);
+// Incremental form of jacobi_svd_batched for 1 < k <= 256 (jacobi_incremental):
+// begin (B = R^T, W = I), any number of jacobi_sweeps launches of up to
+// nsweeps sweeps each (no-ops once converged), end (remaining sweeps +
+// D, Us, Vs).  Lets the caller place the sweeps where SMs are idle.
+bool jacobi_incremental(int k);
+void jacobi_begin(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR, double* work);
+void jacobi_sweeps(cudaStream_t st, int batch, int k, double* work, int nsweeps);
+void jacobi_end(cudaStream_t st, int batch, int k, double* work, double* D, double* Us, double* Vs, int* sweeps_out);
 
 }  // namespace rutv
