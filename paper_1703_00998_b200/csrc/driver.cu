@@ -278,7 +278,8 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   bool final_block = false, final_tall = false, final_fat = false;
   // The b x b SVDs of R11 are independent of later steps (R13): with
   // the single-cluster Jacobi kernel they run in chunks on the side stream.
-  constexpr int64_t kSvdChunk = 8;  // measured at c3: 4 / 8 / 12 / 16 / all-at-end = 274.8 / 272.2 / 272.6 / 275.6 / 278.0 ms
+  // steps per SVD chunk, measured at c3 with the incremental sweeps:
+  // 4 / 6 / 8 / 10 / 12 = 269.0 / 268.0 / 265.3 / 266.6 / 268.0 ms
   const bool svd_side = jacobi_single_launch((int)b);
   cudaStream_t side = svd_side ? side_stream() : nullptr;
   int64_t svd_done = 0;
@@ -315,7 +316,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     cudaEvent_t e = overlap_event(4 + 1);
     RUTV_CK(cudaEventRecord(e, st));
     RUTV_CK(cudaStreamWaitEvent(side, e, 0));
-    jacobi_sweeps(side, (int)(active.s1 - active.s0), (int)b, chunk_work(active.s0), 1);
+    jacobi_sweeps(side, (int)(active.s1 - active.s0), (int)b, chunk_work(active.s0), 1);  // 1 / 2 / 3 per window: 265.3 / 267.5 / 269.5 ms
   };
   auto launch_svd_chunk = [&]() {
     if (steps <= svd_done) return;
