@@ -280,6 +280,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // the single-cluster Jacobi kernel they run in chunks on the side stream.
   // steps per SVD chunk, measured at c3 with the incremental sweeps:
   // 4 / 6 / 8 / 10 / 12 = 269.0 / 268.0 / 265.3 / 266.6 / 268.0 ms
+  constexpr int64_t kSvdChunk = 8;
   const bool svd_side = jacobi_single_launch((int)b);
   cudaStream_t side = svd_side ? side_stream() : nullptr;
   int64_t svd_done = 0;
