@@ -390,6 +390,7 @@ class DistFactor {
     if (ev_fork2_) cudaEventDestroy(ev_fork2_);
     if (ev_join2_) cudaEventDestroy(ev_join2_);
     if (ev_yflags_) cudaEventDestroy(ev_yflags_);
+    if (ev_sweep_) cudaEventDestroy(ev_sweep_);
     if (h_yflags_) cudaFreeHost(h_yflags_);
   }
 
@@ -410,6 +411,7 @@ class DistFactor {
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;  // owner's right-apply overlap
   cudaEvent_t ev_fork2_ = nullptr, ev_join2_ = nullptr;  // owner's panel QR on the priority stream
   cudaEvent_t ev_yflags_ = nullptr;  // the step's sketch-side decision flags are on the host
+  cudaEvent_t ev_sweep_ = nullptr;   // start of a QR chain: an SVD sweep may run beside it
   int* h_yflags_ = nullptr;          // pinned
   std::vector<int> nflags_;  // per local rank: optimistic flag slots used
   // number of steps si < s with si = r (mod P), i.e. the slot of the next owned step
@@ -544,6 +546,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   if (!ev_fork2_) RUTV_CK(cudaEventCreateWithFlags(&ev_fork2_, cudaEventDisableTiming));
   if (!ev_join2_) RUTV_CK(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
   if (!ev_yflags_) RUTV_CK(cudaEventCreateWithFlags(&ev_yflags_, cudaEventDisableTiming));
+  if (!ev_sweep_) RUTV_CK(cudaEventCreateWithFlags(&ev_sweep_, cudaEventDisableTiming));
   if (!h_yflags_) RUTV_CK(cudaMallocHost(&h_yflags_, sizeof(int) * kDistYFlags));
 
   // ---- T <- A, ||A||_F^2 and the non-finite flag (allreduced)
@@ -597,26 +600,80 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   std::vector<SvdChunk> chunks;
   std::vector<cudaEvent_t> evs;
   int64_t svd_done = 0;
+  // incremental SVDs (k <= 256): as in the single-GPU driver, a chunk
+  // advances one sweep at the start of each QR chain of the following steps
+  const bool svd_incr = svd_side && jacobi_incremental((int)b);
+  struct ActiveChunk {
+    int64_t s0 = 0, s1 = 0;
+    bool on = false;
+  } active;
+  auto own_range = [&](const LocalRank& lr, int64_t s0, int64_t s1, int64_t& j0, int64_t& j1) {
+    j0 = own_slot(s0, lr.r);  // this rank's own blocks: steps si = r (mod P), slot j = si / P
+    j1 = own_slot(s1, lr.r);
+  };
+  auto finish_active = [&]() {
+    if (!active.on) return;
+    for (auto& lr : L) {
+      int64_t j0, j1;
+      own_range(lr, active.s0, active.s1, j0, j1);
+      if (j1 > j0)
+        jacobi_end(side, (int)(j1 - j0), (int)b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b),
+                   lr.w.Dall + j0 * b, lr.w.Usall + size_t(j0) * b * b, lr.w.Vsall + size_t(j0) * b * b,
+                   lr.w.sweeps + j0);
+    }
+    cudaEvent_t done;
+    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    evs.push_back(done);
+    RUTV_CK(cudaEventRecord(done, side));
+    chunks.push_back({active.s0, active.s1, done});
+    active.on = false;
+  };
+  auto svd_sweep_here = [&]() {
+    if (!active.on) return;
+    RUTV_CK(cudaEventRecord(ev_sweep_, st));
+    RUTV_CK(cudaStreamWaitEvent(side, ev_sweep_, 0));
+    for (auto& lr : L) {
+      int64_t j0, j1;
+      own_range(lr, active.s0, active.s1, j0, j1);
+      if (j1 > j0) jacobi_sweeps(side, (int)(j1 - j0), (int)b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b), 1);
+    }
+  };
   auto launch_svd_chunk = [&]() {
     if (steps <= svd_done) return;
-    cudaEvent_t fork, done;
+    cudaEvent_t fork;
     RUTV_CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     evs.push_back(fork);
-    evs.push_back(done);
     RUTV_CK(cudaEventRecord(fork, st));
     RUTV_CK(cudaStreamWaitEvent(side, fork, 0));
     const int64_t s0 = svd_done, s1 = steps;
-    for (auto& lr : L) {  // this rank's own blocks only: steps si = r (mod P), slot j = si / P
-      const int64_t j0 = own_slot(s0, lr.r), j1 = own_slot(s1, lr.r);
-      if (j1 > j0)
-        jacobi_svd_batched(side, (int)(j1 - j0), (int)b, lr.w.Rall + size_t(j0 * P + lr.r) * b * b, b,
-                           int64_t(P) * b * b, lr.w.Dall + j0 * b, lr.w.Usall + size_t(j0) * b * b,
-                           lr.w.Vsall + size_t(j0) * b * b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b),
-                           lr.w.sweeps + j0);
+    if (svd_incr) {
+      finish_active();
+      for (auto& lr : L) {
+        int64_t j0, j1;
+        own_range(lr, s0, s1, j0, j1);
+        if (j1 > j0)
+          jacobi_begin(side, (int)(j1 - j0), (int)b, lr.w.Rall + size_t(j0 * P + lr.r) * b * b, b,
+                       int64_t(P) * b * b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b));
+      }
+      active.s0 = s0;
+      active.s1 = s1;
+      active.on = true;
+    } else {
+      for (auto& lr : L) {
+        int64_t j0, j1;
+        own_range(lr, s0, s1, j0, j1);
+        if (j1 > j0)
+          jacobi_svd_batched(side, (int)(j1 - j0), (int)b, lr.w.Rall + size_t(j0 * P + lr.r) * b * b, b,
+                             int64_t(P) * b * b, lr.w.Dall + j0 * b, lr.w.Usall + size_t(j0) * b * b,
+                             lr.w.Vsall + size_t(j0) * b * b, lr.w.jwork + jacobi_work_elems((int)j0, (int)b),
+                             lr.w.sweeps + j0);
+      }
+      cudaEvent_t done;
+      RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      evs.push_back(done);
+      RUTV_CK(cudaEventRecord(done, side));
+      chunks.push_back({s0, s1, done});
     }
-    RUTV_CK(cudaEventRecord(done, side));
-    chunks.push_back({s0, steps, done});
     svd_done = steps;
   };
   auto drop_events = [&]() {
@@ -655,6 +712,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         for (int it = 0; it < q; ++it) {
           if (reortho) {
             set_gemm_role(C_GEMM_QR);
+            svd_sweep_here();
             dist_gram_chol(&RankWork::Y, nt, 1);
             bool ok;
             if (opt_y && ny < kDistYFlags) {  // decision flags on the device, read after QR(Y)
@@ -697,6 +755,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         set_gemm_role(C_GEMM_QR);
         for (size_t l = 0; l < L.size(); ++l) Tv[l] = L[l].w.Tfin;  // T_v of this step
         bool qr_ok = false;
+        svd_sweep_here();
         if (o.qr_mode == 0) {
           dist_gram_chol(&RankWork::Y, nt, 1);
           for (size_t l = 0; l < L.size(); ++l) {
@@ -924,6 +983,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   set_gemm_role(C_GEMM_OTHER);
   if (svd_side) {
     launch_svd_chunk();
+    finish_active();
   } else if (steps > 0) {
     for (auto& lr : L) {
       const int64_t j1 = own_slot(steps, lr.r);
