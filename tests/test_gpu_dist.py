@@ -159,3 +159,32 @@ def test_dist_uv_factorization(m, n, b, q, nranks, kw):
     # the T-only distributed run gives the same T to rounding
     T0, _ = run_dist(A, nranks, b, q, 7, **kw)
     np.testing.assert_allclose(T, T0, rtol=0, atol=1e-12 * a)
+
+
+_drng = np.random.default_rng(7)
+DIST_FUZZ = []
+for _ in range(12):
+    n = int(_drng.integers(8, 300))
+    m = n + int(_drng.integers(0, 200))
+    DIST_FUZZ.append((m, n, int(_drng.choice([4, 16, 33, 64])), int(_drng.integers(0, 3)), int(_drng.integers(1, 6)),
+                      bool(_drng.integers(0, 2)), int(_drng.integers(0, 2**31))))
+
+
+@pytest.mark.parametrize("m,n,b,q,nranks,uv,seed", DIST_FUZZ)
+def test_dist_fuzz(m, n, b, q, nranks, uv, seed):
+    """Random shapes, block widths and rank counts through the loopback
+    communicator: T against the oracle's parity rule; with U, V the exact
+    invariants."""
+    A = testmat.gaussian(m, n, seed % 1000)
+    ref = oracle.randutv(A, min(b, n), q, seed, build_ortho=False)
+    if uv:
+        U, T, V, info = run_dist_uv(A, nranks, b, q, seed)
+        a = np.linalg.norm(A)
+        assert np.linalg.norm(A - U @ T @ V.T) <= 1e-13 * m * a
+        assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-13 * m
+        assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-13 * m
+    else:
+        T, info = run_dist(A, nranks, b, q, seed)
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert np.all(np.tril(T, -1) == 0.0)
