@@ -624,7 +624,12 @@ bool jacobi_single_launch(int k) {
   return k > 1 && d.nb / 2 <= MAX_CLUSTER;
 }
 
-size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 1); }
+// per matrix: B and W (k x k each) and MAX_SWEEPS + 2 int slots (sweep counts,
+// next-sweep index) padded to MAX_SWEEPS + 2 doubles -- an even count, so that
+// jacobi_work_elems(j0, k) is a 16-byte aligned offset for any j0 (callers
+// carve sub-batches starting at matrix j0; the k-even block I/O is 16-byte)
+static_assert((MAX_SWEEPS + 2) % 2 == 0, "16-byte aligned sub-batch offsets");
+size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 2); }
 
 namespace {
 // up to max_sweeps sweeps of jacobi_cluster2_k on every matrix of the batch
