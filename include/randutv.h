@@ -231,9 +231,12 @@ RANDUTV_API int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_
  * return each shard holds that rank's columns of U, T, V; info is identical on
  * all ranks.  Errors: -1 opts, -2 comm, -3 m, -4 n (n > m unsupported here),
  * -5 A_loc/lda_loc, -7 b, -8 q, -10 k_stop, -12 U_loc/ldu_loc, -13
- * T_loc/ldt_loc, -16 V_loc/ldv_loc (or only one of U/V given);
- * RANDUTV_ERR_UNSUPPORTED for opts->oversample > 0; RANDUTV_ERR_NCCL on a
- * failed collective.  Synchronises the stream as randutv_factor_ex does. */
+ * T_loc/ldt_loc, -16 V_loc/ldv_loc (or only one of U/V given), -1 also for
+ * b + opts->oversample > RANDUTV_MAX_B; RANDUTV_ERR_NCCL on a failed
+ * collective.  Over-sampling (opts->oversample = p > 0, Remark
+ * remark:positivep): the b + p_i column sketch is row-distributed like Y; its
+ * projection Z = Q U_R(:, 1:b) is computed redundantly on every rank from the
+ * allgathered sketch (Householder QR + Jacobi SVD of R).  Synchronises the stream as randutv_factor_ex does. */
 RANDUTV_API int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m, int64_t n,
                                     const double* const* A_loc, const int64_t* lda_loc, int64_t b, int32_t q,
                                     uint64_t seed, int64_t k_stop, double* const* U_loc, const int64_t* ldu_loc,

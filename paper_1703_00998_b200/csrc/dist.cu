@@ -227,6 +227,7 @@ struct RankWork {
   double *Rall, *Dall, *Usall, *Vsall, *jwork;
   double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf, *Tfin, *tau, *Ttmp, *Rtmp;
   double *piece, *gath, *Yfull, *scal, *nrm;
+  double *Ro, *Do, *Uso, *Vso, *jworko;  // over-sampling (R23): R of the gathered Y', its SVD
   // U, V formation (DistPlan::uv): replicated W_u / T_u / T_v of every step,
   // this rank's rows of every W_v
   double *Wu_all, *Tu_all, *Wvl_all, *Tv_all;
@@ -240,6 +241,7 @@ struct RankWork {
 
 struct DistPlan {
   int64_t m, n, b, s, nrand, nl_max, maxpiece;
+  int64_t bs;  // sketch width b + p (over-sampling p, R23)
   int P;
   bool uv = false;
   std::vector<size_t> off_u, off_vl;  // per step: offsets into Wu_all (m_i x b) / Wvl_all (piece_i x b)
@@ -256,19 +258,19 @@ inline int64_t max_piece(int64_t n, int64_t b, int64_t p, int P) {
 RankWork carve_rank(Arena& ar, const DistPlan& d) {
   RankWork w{};
   const int64_t m = d.m, b = d.b, nl = std::max<int64_t>(d.nl_max, 1), mx = std::max(m, d.n);
-  const int64_t sb = std::max<int64_t>(d.nrand, 1);
-  w.G = ar.take<double>(size_t(m) * b);
-  w.Y = ar.take<double>(size_t(nl) * b);
-  w.Y2 = ar.take<double>(size_t(nl) * b);
-  w.Z = ar.take<double>(size_t(m) * b);
+  const int64_t sb = std::max<int64_t>(d.nrand, 1), bs = d.bs;
+  w.G = ar.take<double>(size_t(m) * bs);
+  w.Y = ar.take<double>(size_t(nl) * bs);
+  w.Y2 = ar.take<double>(size_t(nl) * bs);
+  w.Z = ar.take<double>(size_t(m) * bs);
   w.P = ar.take<double>(size_t(m) * b);
   w.P2 = ar.take<double>(size_t(m) * b);
   w.S = ar.take<double>(size_t(nl) * b);
   w.S2 = ar.take<double>(size_t(nl) * b);
-  w.pack = ar.take<double>(size_t(m) * b + 2 * size_t(b) * b + 64);
-  w.q1 = ar.take<double>(size_t(mx) * b);
-  w.small = ar.take<double>(small_work_elems(b));
-  w.part_elems = size_t(12) * mx * b + size_t(148) * 32 * 1024;
+  w.pack = ar.take<double>(std::max(size_t(m) * b + 2 * size_t(b) * b, size_t(bs) * bs) + 64);
+  w.q1 = ar.take<double>(size_t(mx) * bs);
+  w.small = ar.take<double>(small_work_elems(bs));
+  w.part_elems = size_t(12) * mx * bs + size_t(148) * 32 * 1024;
   w.part = ar.take<double>(w.part_elems);
   w.fold = ar.take<double>(size_t(mx) * b);
   w.Rall = ar.take<double>(size_t(sb) * b * b);
@@ -282,12 +284,19 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.Vsfin = ar.take<double>(size_t(b) * b);
   w.jworkf = ar.take<double>(jacobi_work_elems(1, (int)b));
   w.Tfin = ar.take<double>(size_t(b) * b);
-  w.tau = ar.take<double>(size_t(b));
-  w.Ttmp = ar.take<double>(size_t(b) * b);
-  w.Rtmp = ar.take<double>(size_t(b) * b);
-  w.piece = ar.take<double>(size_t(d.maxpiece) * b + 1);
-  w.gath = ar.take<double>(size_t(d.P) * d.maxpiece * b + 1);
-  w.Yfull = ar.take<double>(size_t(d.n) * b);
+  w.tau = ar.take<double>(size_t(bs));
+  w.Ttmp = ar.take<double>(size_t(bs) * bs);
+  w.Rtmp = ar.take<double>(size_t(bs) * bs);
+  w.piece = ar.take<double>(size_t(d.maxpiece) * bs + 1);
+  w.gath = ar.take<double>(size_t(d.P) * d.maxpiece * bs + 1);
+  w.Yfull = ar.take<double>(size_t(d.n) * bs);
+  if (bs > b) {
+    w.Ro = ar.take<double>(size_t(bs) * bs);
+    w.Do = ar.take<double>(size_t(bs));
+    w.Uso = ar.take<double>(size_t(bs) * bs);
+    w.Vso = ar.take<double>(size_t(bs) * bs);
+    w.jworko = ar.take<double>(jacobi_work_elems(1, (int)bs));
+  }
   w.scal = ar.take<double>(16);
   w.nrm = ar.take<double>(8192);
   if (d.uv) {
@@ -302,21 +311,22 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.qflags = ar.take<int>(size_t(w.qflags_cap) + kDistYFlags);  // + one step's sketch-side decisions
   w.qw.part = w.part;
   w.qw.part_elems = w.part_elems;
-  w.qw.sfull = ar.take<double>(size_t(32) * b);
-  w.qw.s2 = ar.take<double>(size_t(32) * b);
-  w.qw.z = ar.take<double>(size_t(32) * b);
+  w.qw.sfull = ar.take<double>(size_t(32) * bs);
+  w.qw.s2 = ar.take<double>(size_t(32) * bs);
+  w.qw.z = ar.take<double>(size_t(32) * bs);
   w.qw.q1 = w.q1;
-  w.qw.q1_elems = size_t(mx) * b;
+  w.qw.q1_elems = size_t(mx) * bs;
   w.qw.small = w.small;
   return w;
 }
 
-DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P, bool uv) {
+DistPlan make_dist_plan(int64_t m, int64_t n, int64_t b, int P, bool uv, int64_t ovs = 0) {
   DistPlan d;
   d.uv = uv;
   d.m = m;
   d.n = n;
   d.b = b;
+  d.bs = b + ovs;
   d.P = P;
   d.s = std::min(cdiv(m, b), cdiv(n, b));
   d.nrand = 0;
@@ -422,22 +432,69 @@ class DistFactor {
     return v;
   }
 
-  // Gram of the distributed n_i x b matrix held in `src` (local rows nt) -> W1 of
+  // Gram of the distributed n_i x wd matrix held in `src` (local rows nt) -> W1 of
   // every rank's small workspace (allreduced), then chol_inv (redundant).
-  void dist_gram_chol(double* RankWork::*src, const std::vector<int64_t>& nt, int which /*1: W1, 2: W2*/) {
-    const int bp = small_pad(b);
-    for (size_t l = 0; l < L.size(); ++l) {  // packed b x b (ld b) Gram, allreduced, then into the padded slot
+  // wd = b, or the over-sampled sketch width b + p_i (R23) with the small
+  // workspace carved for that width (small_of).
+  void dist_gram_chol(double* RankWork::*src, const std::vector<int64_t>& nt, int which /*1: W1, 2: W2*/,
+                      int64_t wd) {
+    for (size_t l = 0; l < L.size(); ++l) {  // packed wd x wd (ld wd) Gram, allreduced, then into the padded slot
       auto& lr = L[l];
-      dg(lr.w, st, true, false, b, b, nt[l], 1.0, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.*src,
-         std::max<int64_t>(nt[l], 1), 0.0, lr.w.pack, b);
+      dg(lr.w, st, true, false, wd, wd, nt[l], 1.0, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.*src,
+         std::max<int64_t>(nt[l], 1), 0.0, lr.w.pack, wd);
     }
-    comm.allreduce(bufs(&RankWork::pack), size_t(b) * b, st);
+    comm.allreduce(bufs(&RankWork::pack), size_t(wd) * wd, st);
     for (auto& lr : L) {
-      double* dst = (which == 1) ? lr.sw.W1 : lr.sw.W2;
-      copy_matrix(st, b, b, lr.w.pack, b, dst, bp);
+      const SmallWork sw = small_of(lr, wd);
+      copy_matrix(st, wd, wd, lr.w.pack, wd, (which == 1) ? sw.W1 : sw.W2, sw.bp);
     }
     if (which == 1)
-      for (auto& lr : L) small_chol_inv(st, b, lr.sw);
+      for (auto& lr : L) small_chol_inv(st, wd, small_of(lr, wd));
+  }
+  static SmallWork small_of(const LocalRank& lr, int64_t wd) { return carve_small(lr.w.small, wd); }
+
+  // the distributed n_i x wd matrix in `src` (local rows nt) -> Yfull (n_i x wd,
+  // ld n_i) on every rank: padded allgather of the row pieces
+  void gather_full(int64_t p, int64_t ni, int64_t wd, double* RankWork::*src, const std::vector<int64_t>& nt) {
+    const int64_t maxpiece = max_piece(n, b, p, P);
+    for (size_t l = 0; l < L.size(); ++l) {
+      auto& lr = L[l];
+      set_zero(st, maxpiece, wd, lr.w.piece, maxpiece);
+      copy_matrix(st, nt[l], wd, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.piece, maxpiece);
+    }
+    comm.allgather(bufs(&RankWork::piece), bufs(&RankWork::gath), size_t(maxpiece) * wd, st);
+    for (auto& lr : L) {
+      ProfScope _p(st, K_MISC, 0.0);
+      count_launch(K_MISC);
+      gather_rows_k<<<grid_for_n(ni * wd), 256, 0, st>>>(ni, wd, b, p, P, lr.w.gath, maxpiece, lr.w.Yfull, ni);
+      RUTV_LAUNCH_CK();
+    }
+  }
+
+  // Over-sampling (R23; Fig. fig:stepUTVoversampling ``[Z,~,~] = svd(Y,'econ')``):
+  // the distributed n_i x (b + p_i) sketch Y' in Y -> Y (local rows) = the rows
+  // of Z = Q U_R(:, 1:b), with Y' = Q R and R = U_R D V_R^T computed redundantly
+  // on every rank from the gathered Y' (the same kernels on the same data, so
+  // every rank holds the same Z).  Householder panels: Y' after the power
+  // iteration can be far too ill-conditioned for CholeskyQR.
+  int dist_oversample(int64_t p, int64_t ni, int64_t wd, const std::vector<int64_t>& nt) {
+    gather_full(p, ni, wd, &RankWork::Y, nt);
+    for (size_t l = 0; l < L.size(); ++l) {
+      auto& lr = L[l];
+      QrWork qw = lr.w.qw;
+      qw.mode = 1;
+      int rc = panel_qr(st, ni, wd, lr.w.Yfull, ni, lr.w.Ro, wd, lr.w.tau, lr.w.Ttmp, wd, qw);
+      if (rc != OK) return rc;
+      thin_q(st, ni, wd, lr.w.Yfull, ni, lr.w.Ttmp, wd, lr.w.q1, ni, lr.w.Rtmp, lr.w.part, lr.w.part_elems);
+      jacobi_svd_batched(st, 1, (int)wd, lr.w.Ro, wd, wd * wd, lr.w.Do, lr.w.Uso, lr.w.Vso, lr.w.jworko, nullptr);
+      dg(lr.w, st, false, false, ni, b, wd, 1.0, lr.w.q1, ni, lr.w.Uso, wd, 0.0, lr.w.Yfull, ni);
+      ProfScope _p(st, K_MISC, 0.0);
+      count_launch(K_MISC);
+      scatter_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.r, lr.w.Yfull, ni, lr.w.Y,
+                                                          std::max<int64_t>(nt[l], 1));
+      RUTV_LAUNCH_CK();
+    }
+    return OK;
   }
 
   // Householder fallback for a distributed Y: allgather -> full Y on every rank,
@@ -449,39 +506,26 @@ class DistFactor {
   // update is rank-local; W_v is row-distributed and is allgathered per step.
   void form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf);
 
+  // wd: column count (b; b + p_i for an over-sampled re-orthonormalization, mode 0)
   int dist_householder(int64_t p, int64_t ni, double* RankWork::*src, double* RankWork::*dst,
-                       const std::vector<int64_t>& nt, int mode, double* const* Tv) {
-    int64_t maxpiece = 0;
-    for (int r = 0; r < P; ++r) maxpiece = std::max(maxpiece, local_cols(n, b, r, P) - b * blocks_before(p, r, P));
-    maxpiece = std::max<int64_t>(maxpiece, 1);
+                       const std::vector<int64_t>& nt, int mode, double* const* Tv, int64_t wd) {
+    gather_full(p, ni, wd, src, nt);
     for (size_t l = 0; l < L.size(); ++l) {
       auto& lr = L[l];
-      set_zero(st, maxpiece, b, lr.w.piece, maxpiece);
-      copy_matrix(st, nt[l], b, lr.w.*src, std::max<int64_t>(nt[l], 1), lr.w.piece, maxpiece);
-    }
-    comm.allgather(bufs(&RankWork::piece), bufs(&RankWork::gath), size_t(maxpiece) * b, st);
-    for (size_t l = 0; l < L.size(); ++l) {
-      auto& lr = L[l];
-      {
-        ProfScope _p(st, K_MISC, 0.0);
-        count_launch(K_MISC);
-        gather_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.w.gath, maxpiece, lr.w.Yfull, ni);
-        RUTV_LAUNCH_CK();
-      }
       QrWork qw = lr.w.qw;
       qw.mode = 1;
-      int rc = panel_qr(st, ni, b, lr.w.Yfull, ni, lr.w.Rtmp, b, lr.w.tau, mode == 1 ? Tv[l] : lr.w.Ttmp, b, qw);
+      int rc = panel_qr(st, ni, wd, lr.w.Yfull, ni, lr.w.Rtmp, wd, lr.w.tau, mode == 1 ? Tv[l] : lr.w.Ttmp, wd, qw);
       if (rc != OK) return rc;
       double* out = lr.w.Yfull;
-      if (mode == 0) {  // thin Q into q1 (ni x b), then scatter
-        thin_q(st, ni, b, lr.w.Yfull, ni, lr.w.Ttmp, b, lr.w.q1, ni, lr.w.Rtmp, lr.w.part, lr.w.part_elems);
+      if (mode == 0) {  // thin Q into q1 (ni x wd), then scatter
+        thin_q(st, ni, wd, lr.w.Yfull, ni, lr.w.Ttmp, wd, lr.w.q1, ni, lr.w.Rtmp, lr.w.part, lr.w.part_elems);
         out = lr.w.q1;
       }
       {
         ProfScope _p(st, K_MISC, 0.0);
         count_launch(K_MISC);
-        scatter_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.r, out, ni, lr.w.*dst,
-                                                            std::max<int64_t>(nt[l], 1));
+        scatter_rows_k<<<grid_for_n(ni * wd), 256, 0, st>>>(ni, wd, b, p, P, lr.r, out, ni, lr.w.*dst,
+                                                             std::max<int64_t>(nt[l], 1));
         RUTV_LAUNCH_CK();
       }
     }
@@ -701,39 +745,42 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       int lam_err = OK;
       auto sketch_qr_p = [&](bool opt_y) -> int {
         int ny = 0;
-        // ---- sketch
+        // ---- sketch; over-sampled to b + p_i columns (R23)
+        const int64_t p_i = std::min<int64_t>(o.oversample, ni - b);
+        const int64_t bw = b + p_i;
         set_gemm_role(C_GEMM_SKETCH);
         for (size_t l = 0; l < L.size(); ++l) {
           auto& lr = L[l];
-          gaussian_fill(st, lr.w.G, m, mi, b, seed, uint32_t(p), 0u);
-          dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.G, m, 0.0, lr.w.Y,
+          gaussian_fill(st, lr.w.G, m, mi, bw, seed, uint32_t(p), 0u);
+          dg(lr.w, st, true, false, nt[l], bw, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.G, m, 0.0, lr.w.Y,
              std::max<int64_t>(nt[l], 1));
         }
         for (int it = 0; it < q; ++it) {
           if (reortho) {
             set_gemm_role(C_GEMM_QR);
             svd_sweep_here();
-            dist_gram_chol(&RankWork::Y, nt, 1);
+            dist_gram_chol(&RankWork::Y, nt, 1, bw);
             bool ok;
             if (opt_y && ny < kDistYFlags) {  // decision flags on the device, read after QR(Y)
               for (size_t l = 0; l < L.size(); ++l)
-                reortho_flag(st, L[l].sw.stats, 1e4, L[l].w.qflags + L[l].w.qflags_cap + ny);
+                reortho_flag(st, small_of(L[l], bw).stats, 1e4, L[l].w.qflags + L[l].w.qflags_cap + ny);
               ++ny;
               ok = true;
             } else {
               double h[3];
-              RUTV_CK(cudaMemcpyAsync(h, L[0].sw.stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+              RUTV_CK(cudaMemcpyAsync(h, small_of(L[0], bw).stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
               RUTV_CK(cudaStreamSynchronize(st));
               ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
             }
             if (ok) {
               for (size_t l = 0; l < L.size(); ++l) {
                 auto& lr = L[l];
-                dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
-                   lr.w.Y2, std::max<int64_t>(nt[l], 1), true);
+                const SmallWork sw = small_of(lr, bw);
+                dg(lr.w, st, false, false, nt[l], bw, bw, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), sw.R1i, sw.bp,
+                   0.0, lr.w.Y2, std::max<int64_t>(nt[l], 1), true);
               }
             } else {
-              int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr);
+              int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 0, nullptr, bw);
               if (rc != OK) { lam_err = rc; return -1; }
             }
             for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
@@ -741,15 +788,20 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           }
           for (size_t l = 0; l < L.size(); ++l) {  // Z = X Y  (partial)
             auto& lr = L[l];
-            dg(lr.w, st, false, false, mi, b, nt[l], 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
+            dg(lr.w, st, false, false, mi, bw, nt[l], 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y,
                std::max<int64_t>(nt[l], 1), 0.0, lr.w.Z, mi);
           }
-          comm.allreduce(bufs(&RankWork::Z), size_t(mi) * b, st);
+          comm.allreduce(bufs(&RankWork::Z), size_t(mi) * bw, st);
           for (size_t l = 0; l < L.size(); ++l) {  // Y = X^T Z
             auto& lr = L[l];
-            dg(lr.w, st, true, false, nt[l], b, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Z, mi, 0.0,
+            dg(lr.w, st, true, false, nt[l], bw, mi, 1.0, lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Z, mi, 0.0,
                lr.w.Y, std::max<int64_t>(nt[l], 1));
           }
+        }
+        if (p_i > 0) {  // Y <- the rows of Z = Q U_R(:, 1:b) (R23)
+          set_gemm_role(C_GEMM_QR);
+          int rc = dist_oversample(p, ni, bw, nt);
+          if (rc != OK) { lam_err = rc; return -1; }
         }
         // ---- QR(Y) -> W_v (rows distributed), T_v
         set_gemm_role(C_GEMM_QR);
@@ -757,13 +809,13 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         bool qr_ok = false;
         svd_sweep_here();
         if (o.qr_mode == 0) {
-          dist_gram_chol(&RankWork::Y, nt, 1);
+          dist_gram_chol(&RankWork::Y, nt, 1, b);
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
             dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
                lr.w.q1, std::max<int64_t>(nt[l], 1), true);
           }
-          dist_gram_chol(&RankWork::q1, nt, 2);
+          dist_gram_chol(&RankWork::q1, nt, 2, b);
           // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
@@ -789,7 +841,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           }
         }
         if (!qr_ok) {
-          int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 1, Tv.data());
+          int rc = dist_householder(p, ni, &RankWork::Y, &RankWork::Y2, nt, 1, Tv.data(), b);
           if (rc != OK) { lam_err = rc; return -1; }
           for (auto& lr : L) std::swap(lr.w.Y, lr.w.Y2);
         }
@@ -1261,7 +1313,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   randutv_opts o{};
   if (opts) o = *opts;
   if (o.tol < 0 || std::isnan(o.tol) || o.qr_mode < 0 || o.qr_mode > 1 || o.oversample < 0) return -1;
-  if (o.oversample > 0) return RANDUTV_ERR_UNSUPPORTED;  // over-sampling: single-GPU path only
+  if (b + o.oversample > RANDUTV_MAX_B) return -1;
   if (b > n) b = n;
   rutv::Comm& c = *comm->c;
   const int nlr = (int)c.ranks.size();
@@ -1274,7 +1326,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   }
   std::lock_guard<std::mutex> lock(rutv::g_dmu);
   try {
-    rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P, uv);
+    rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P, uv, o.oversample);
     const size_t per = rutv::dist_rank_bytes(d);
     char* ws = (char*)rutv::dist_ws(per * nlr);
     if (!ws) return RANDUTV_ERR_NOMEM;

@@ -142,7 +142,8 @@ def nccl_from_torch(group=None) -> Comm:
 
 # --------------------------------------------------------------------------- the factorization
 def factor(comm: Comm, shards, m: int, n: int, b: int, q: int, seed: int, k_stop: int = 0, tol: float = 0.0,
-           reortho: bool = True, qr_mode: int = 0, out=None, stream=None, with_uv: bool = False):
+           reortho: bool = True, qr_mode: int = 0, out=None, stream=None, with_uv: bool = False,
+           oversample: int = 0):
     """Distributed A = U T V^T.  ``shards``: one column-major CUDA tensor per
     rank driven by ``comm`` (comm.ranks order), rank r's shard being
     m x local_cols(n, b, r, P).  Returns (T shards, Info), or with ``with_uv``
@@ -168,7 +169,7 @@ def factor(comm: Comm, shards, m: int, n: int, b: int, q: int, seed: int, k_stop
         ldu = (c_i64 * nl)(*[_ld(U) for U in Us])
         ldv = (c_i64 * nl)(*[_ld(V) for V in Vs])
     opts = _Opts(stream=_stream(stream, shards[0].device).value, tol=float(tol), no_reortho=0 if reortho else 1,
-                 qr_mode=int(qr_mode))
+                 qr_mode=int(qr_mode), oversample=int(oversample))
     info = _Info()
     rc = L.randutv_factor_dist(ctypes.byref(opts), comm.h, m, n, Ap, lda, int(b), int(q), int(seed) & (2**64 - 1),
                                int(k_stop), Up, ldu, Tp, ldt, Vp, ldv, ctypes.byref(info))

@@ -380,6 +380,11 @@ def test_poisoned_workspace_initcheck():
             Us, Ts, Vs, _ = D_.factor(comm, sh, 700, 520, 64, 1, 2, with_uv=True)
             comm.close()
             out += [D_.assemble(Us, 700, 64), D_.assemble(Ts, 520, 64), D_.assemble(Vs, 520, 64)]
+            comm = D_.loopback(2)
+            sh = [D_.shard(to_dev(A2), 64, r, 2) for r in range(2)]
+            Ts, _ = D_.factor(comm, sh, 700, 520, 64, 2, 3, oversample=6)
+            comm.close()
+            out += [D_.assemble(Ts, 520, 64)]
             torch.cuda.synchronize()
             runs.append([to_host(x) for x in out])
         finally:
