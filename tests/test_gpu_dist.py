@@ -268,3 +268,33 @@ def test_dist_svd_chunk_slot_alignment(m, n, b, nranks):
     assert info.steps == ref["steps"] and info.steps > 8
     par = check_parity(T, ref["T"], ref["a_fro"])
     assert par["diag_ok"] and par["ek_ok"], par
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_dist_weak_scaling_shapes_loopback(nranks):
+    """The exact matrices `bench.py --gpus N` factors at N = 2, 4, 8 (weak
+    scaling: the c3 recipe at n = 10000 N^(1/3)), through the multi-GPU
+    algorithm with N virtual ranks on one GPU: the same T diagonal as the
+    single-GPU factorization (which test_gpu_fullsize pins to the oracle at
+    full size) to rounding, exact triangularity and ||T||_F = ||A||_F."""
+    At, c = testmat.device_config("c3", scale=nranks ** (1.0 / 3.0))
+    A = At.t()
+    m, n = A.shape
+    comm = D.loopback(nranks)
+    shards = [D.shard(A, c.b, r, nranks) for r in range(nranks)]
+    Ts, info = D.factor(comm, shards, m, n, c.b, c.q, c.seed)
+    torch.cuda.synchronize()
+    comm.close()
+    del shards
+    T = D.assemble(Ts, n, c.b)
+    del Ts
+    assert info.k_done == n
+    a = torch.linalg.norm(A).item()
+    assert abs(torch.linalg.norm(T).item() - a) <= 4 * n * EPS * a
+    assert not torch.any(torch.tril(T, -1) != 0).item()
+    dd = torch.diagonal(T).abs().cpu().numpy()
+    del T
+    _, T1, _, _ = P.randutv(A, c.b, c.q, c.seed, with_uv=False)
+    torch.cuda.synchronize()
+    d1 = torch.diagonal(T1).abs().cpu().numpy()
+    assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * a)
