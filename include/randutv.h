@@ -61,8 +61,8 @@ typedef struct randutv_opts {
                              PAPER.md:1124-1142; Fig. fig:stepUTVoversampling): G has
                              b + p_i columns, p_i = min(p, n_i - b), and QR(Y) acts on the
                              b dominant left singular vectors of the extended Y.  0 = the
-                             paper's Fig. fig:randUTV.  b + p <= RANDUTV_MAX_B.  Single-GPU
-                             entry points only (randutv_factor_dist: RANDUTV_ERR_UNSUPPORTED) */
+                             paper's Fig. fig:randUTV.  b + p <= RANDUTV_MAX_B.  Honoured by
+                             every factorization entry point incl. randutv_factor_dist */
   int32_t reserved1;
 } randutv_opts;
 
