@@ -218,6 +218,17 @@ def test_dist_oversampling_parity(name, scale, q, p, nranks, uv):
     assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * ref["a_fro"])
 
 
+def test_dist_oversampling_householder_reortho():
+    """qr_mode 1: the re-orthonormalizations of the b + p_i column sketch take
+    the allgather + redundant Householder path (width b + p_i), QR(Y) too."""
+    c = testmat.config("c2", scale=0.2, q=2)
+    ref = oracle.randutv(c.A, c.b, c.q, c.seed, build_ortho=False, p=9)
+    T, info = run_dist(c.A, 3, c.b, c.q, c.seed, oversample=9, qr_mode=1)
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert info.qr_fallbacks > 0
+
+
 def test_dist_oversampling_argument_checks():
     A = testmat.gaussian(64, 64, 1)
     with pytest.raises(Exception):
