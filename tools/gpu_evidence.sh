@@ -1,5 +1,5 @@
 #!/bin/bash
-# One gpurun call: GPU tests, the default bench line, GEMM-vs-cuBLAS table,
+# One gpurun call: GPU tests, the default bench line, the --dist bench line (NCCL, 1 rank), GEMM-vs-cuBLAS table,
 # the ncu launch list of one factorization (tools/prof_step.py: 1 warm-up + 1
 # profiled step; the summary keeps the last step's launches) and one full ncu
 # capture of the three dominant GEMM shapes.  Usage (under gpurun):
@@ -11,6 +11,9 @@ timeout 1200 python -m pytest tests -m gpu -q > $O/${TAG}_pytest.log 2>&1; echo 
 tail -3 $O/${TAG}_pytest.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err; echo "bench rc=$?"
 cat $O/${TAG}_bench.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+    --master-port 29513 bench.py --gpus 1 --dist --no-cpu-baseline 2> $O/${TAG}_bench_dist_n1.err | tail -1 \
+    > $O/${TAG}_bench_dist_n1.json; echo "dist bench rc=$?"
 timeout 600 python tools/bench_gemm.py > $O/${TAG}_gemm.log 2>&1; cat $O/${TAG}_gemm.log
 P="python tools/prof_step.py c3 1"
 $P > $O/${TAG}_prof_plain.log 2>&1 && cat $O/${TAG}_prof_plain.log && \
