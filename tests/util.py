@@ -66,13 +66,15 @@ def selection_well_posed(A, b, q, seed, p, ref, k_stop=0):
     (e.g. Gaussian inputs after some steps) it is not, and any rounding
     difference selects a different, equally valid subspace.  Detected from the
     oracle itself: re-run it on A perturbed by 1e-15 relative noise; if its
-    own |diag T| / e_k move beyond the parity rule, the case is ill-posed and
-    only the exact invariants are comparable.  p = 0 is always well posed."""
+    own |diag T| / e_k move beyond 1/100 of the parity rule, the case is
+    treated as ill-posed and only the exact invariants are comparable.  p = 0 is always well posed."""
     import oracle
     if p <= 0:
         return True
     rng = np.random.default_rng(12345)
     A2 = np.asfortranarray(A * (1.0 + 1e-15 * rng.standard_normal(A.shape)))
     r2 = oracle.randutv(A2, b, q, seed, k_stop=k_stop, build_ortho=False, p=p)
-    par = check_parity(r2["T"], ref["T"], ref["a_fro"])
+    # with a 100x margin inside the parity rule: one perturbed sample only
+    # estimates the sensitivity
+    par = check_parity(r2["T"], ref["T"], ref["a_fro"], rtol_diag=1e-12, rtol_ek=1e-10)
     return bool(par["diag_ok"] and par["ek_ok"])
