@@ -497,15 +497,15 @@ class DistFactor {
     return OK;
   }
 
-  // Householder fallback for a distributed Y: allgather -> full Y on every rank,
-  // panel QR there (redundant), then every rank takes its rows of the result.
-  // mode 0: thin Q -> dst (re-orthonormalisation); mode 1: reflectors -> dst, Tv.
   // U = U_1 ... U_s blockdiag(Us_i), V likewise by
   // backward accumulation on each rank's column shards: a block reflector
   // acts on rows, so with W_u replicated (broadcast by the panel owner) the U
   // update is rank-local; W_v is row-distributed and is allgathered per step.
   void form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf);
 
+  // Householder fallback for a distributed Y: allgather -> full Y on every rank,
+  // panel QR there (redundant), then every rank takes its rows of the result.
+  // mode 0: thin Q -> dst (re-orthonormalisation); mode 1: reflectors -> dst, Tv.
   // wd: column count (b; b + p_i for an over-sampled re-orthonormalization, mode 0)
   int dist_householder(int64_t p, int64_t ni, double* RankWork::*src, double* RankWork::*dst,
                        const std::vector<int64_t>& nt, int mode, double* const* Tv, int64_t wd) {
