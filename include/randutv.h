@@ -229,7 +229,9 @@ RANDUTV_API int64_t randutv_dist_global_col(int64_t local_col, int64_t b, int32_
  *                      W_v's row pieces are allgathered once per step at the end.
  * All ranks must pass identical m, n, b, q, seed, k_stop and options.  On
  * return each shard holds that rank's columns of U, T, V; info is identical on
- * all ranks.  Errors: -1 opts, -2 comm, -3 m, -4 n (n > m unsupported here),
+ * all ranks.  Fat inputs (n > m) as on one GPU (Remark "The case m < n"): the
+ * final m_i x n_i block's transpose is allgathered and factored redundantly.
+ * Errors: -1 opts, -2 comm, -3 m, -4 n,
  * -5 A_loc/lda_loc, -7 b, -8 q, -10 k_stop, -12 U_loc/ldu_loc, -13
  * T_loc/ldt_loc, -16 V_loc/ldv_loc (or only one of U/V given), -1 also for
  * b + opts->oversample > RANDUTV_MAX_B; RANDUTV_ERR_NCCL on a failed

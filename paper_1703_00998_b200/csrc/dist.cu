@@ -263,8 +263,8 @@ RankWork carve_rank(Arena& ar, const DistPlan& d) {
   w.Y = ar.take<double>(size_t(nl) * bs);
   w.Y2 = ar.take<double>(size_t(nl) * bs);
   w.Z = ar.take<double>(size_t(m) * bs);
-  w.P = ar.take<double>(size_t(m) * b);
-  w.P2 = ar.take<double>(size_t(m) * b);
+  w.P = ar.take<double>(size_t(mx) * b);  // mx: also k x n_loc scratch of the V formation (fat inputs)
+  w.P2 = ar.take<double>(size_t(mx) * b);
   w.S = ar.take<double>(size_t(nl) * b);
   w.S2 = ar.take<double>(size_t(nl) * b);
   w.pack = ar.take<double>(std::max(size_t(m) * b + 2 * size_t(b) * b, size_t(bs) * bs) + 64);
@@ -501,7 +501,7 @@ class DistFactor {
   // backward accumulation on each rank's column shards: a block reflector
   // acts on rows, so with W_u replicated (broadcast by the panel owner) the U
   // update is rank-local; W_v is row-distributed and is allgathered per step.
-  void form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf);
+  void form_uv(int64_t steps, bool final_block, bool final_fat, int64_t r0f, int64_t mif, int64_t nif, int64_t pf);
 
   // Householder fallback for a distributed Y: allgather -> full Y on every rank,
   // panel QR there (redundant), then every rank takes its rows of the result.
@@ -628,7 +628,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   }
 
   int64_t steps = 0, k_done = 0;
-  bool final_block = false;
+  bool final_block = false, final_fat = false;
   int64_t r0f = 0, mif = 0, nif = 0, pf = 0;
   std::vector<int64_t> nt(L.size()), c0(L.size());
 
@@ -976,6 +976,26 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       mif = mi;
       nif = ni;
       pf = p;
+      if (mi < ni) {
+        // fat (Remark "The case m < n"): unpivoted QR of the ROWS of
+        // X, X^T = Q [Rf; 0].  X^T's rows are X's columns, distributed like Y:
+        // allgather them and factor redundantly on every rank (the same kernels
+        // on the same data: identical reflectors W_f (in Yfull), T_f, R_f).
+        final_fat = true;
+        for (size_t l = 0; l < L.size(); ++l) {
+          auto& lr = L[l];
+          if (nt[l] > 0) transpose_matrix(st, mi, nt[l], lr.T + r0 + c0[l] * lr.ldt, lr.ldt, lr.w.Y, nt[l]);
+        }
+        gather_full(p, ni, mi, &RankWork::Y, nt);
+        for (auto& lr : L) {
+          QrWork qw = lr.w.qw;
+          qw.mode = 1;
+          int rc = panel_qr(st, ni, mi, lr.w.Yfull, ni, lr.w.Rfin, mi, lr.w.tau, lr.w.Tfin, mi, qw);
+          if (rc != OK) return rc;
+        }
+        k_done = m;
+        break;
+      }
       for (size_t l = 0; l < L.size(); ++l) {
         auto& lr = L[l];
         if (lr.r != owner) continue;
@@ -1077,7 +1097,46 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   }
   for (cudaEvent_t e : evs) cudaEventDestroy(e);
   evs.clear();
-  if (final_block) {
+  if (final_block && final_fat) {
+    // T(I2, J) = [diag(D) 0];  T(I1, J) <- T(I1, J) Q blockdiag(Us, I) with
+    // Q = I - W_f T_f W_f^T acting on the columns J (distributed): P = T(I1, J) W_f
+    // from the local columns, allreduced (r0 x m_i), then the local rank-m_i update
+    const int owner = int(pf % P);
+    for (auto& lr : L) {
+      const int64_t cs = b * blocks_before(pf, lr.r, P), nc = lr.nl - cs;
+      if (lr.r == owner)
+        jacobi_svd_batched(st, 1, (int)mif, lr.w.Rfin, mif, mif * mif, lr.w.Dfin, lr.w.Usfin, lr.w.Vsfin,
+                           lr.w.jworkf, lr.w.sweeps + steps);
+      if (nc > 0) set_zero(st, mif, nc, lr.T + r0f + cs * lr.ldt, lr.ldt);
+      if (lr.r == owner) write_diag_block(st, mif, mif, lr.w.Dfin, lr.T + r0f + cs * lr.ldt, lr.ldt);
+    }
+    if (r0f > 0) {
+      for (auto& lr : L) {
+        const int64_t cs = b * blocks_before(pf, lr.r, P), nc = lr.nl - cs;
+        if (nc > 0) {
+          ProfScope _p(st, K_MISC, 0.0);
+          count_launch(K_MISC);
+          scatter_rows_k<<<grid_for_n(nif * mif), 256, 0, st>>>(nif, mif, b, pf, P, lr.r, lr.w.Yfull, nif, lr.w.Y, nc);
+          RUTV_LAUNCH_CK();
+          dg(lr.w, st, false, false, r0f, mif, nc, 1.0, lr.T + cs * lr.ldt, lr.ldt, lr.w.Y, nc, 0.0, lr.w.P, r0f);
+        } else {
+          set_zero(st, r0f, mif, lr.w.P, r0f);
+        }
+      }
+      comm.allreduce(bufs(&RankWork::P), size_t(r0f) * mif, st);
+      for (auto& lr : L) {
+        const int64_t cs = b * blocks_before(pf, lr.r, P), nc = lr.nl - cs;
+        if (nc <= 0) continue;
+        dg(lr.w, st, false, false, r0f, mif, mif, 1.0, lr.w.P, r0f, lr.w.Tfin, mif, 0.0, lr.w.P2, r0f);
+        dg(lr.w, st, false, true, r0f, nc, mif, -1.0, lr.w.P2, r0f, lr.w.Y, nc, 1.0, lr.T + cs * lr.ldt, lr.ldt);
+        if (lr.r == owner) {  // the first m_i columns of J (block pf, on its owner): . Us
+          dg(lr.w, st, false, false, r0f, mif, mif, 1.0, lr.T + cs * lr.ldt, lr.ldt, lr.w.Usfin, mif, 0.0,
+             lr.w.fold, r0f);
+          copy_matrix(st, r0f, mif, lr.w.fold, r0f, lr.T + cs * lr.ldt, lr.ldt);
+        }
+      }
+    }
+  } else if (final_block) {
     const int owner = int(pf % P);
     for (auto& lr : L) {
       if (lr.r != owner) continue;
@@ -1093,7 +1152,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     }
   }
 
-  if (plan_.uv) form_uv(steps, final_block, r0f, mif, nif, pf);
+  if (plan_.uv) form_uv(steps, final_block, final_fat, r0f, mif, nif, pf);
 
   if (info) {
     info->k_done = k_done;
@@ -1119,7 +1178,8 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   return RANDUTV_OK;
 }
 
-void DistFactor::form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t mif, int64_t nif, int64_t pf) {
+void DistFactor::form_uv(int64_t steps, bool final_block, bool final_fat, int64_t r0f, int64_t mif, int64_t nif,
+                         int64_t pf) {
   set_gemm_role(C_GEMM_OTHER);
   for (auto& lr : L) {
     const int64_t mloc = local_cols(m, b, lr.r, P);
@@ -1146,6 +1206,8 @@ void DistFactor::form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t m
     dg(lr.w, st, false, false, k, nc, k, 1.0, Tw, ldtw, lr.w.fold, k, 0.0, lr.w.P, k);
     dg(lr.w, st, false, false, rows, nc, k, -1.0, W, ldw, lr.w.P, k, 1.0, Xb, ldx);
   };
+  if (final_block && final_fat)  // V' <- Q_f V' (W_f, T_f replicated: the redundant QR of X^T)
+    for (auto& lr : L) apply_left(lr, lr.V, lr.ldv, lr.nl, pf, nif, mif, lr.w.Yfull, nif, lr.w.Tfin, mif);
   if (final_block && mif > nif)
     for (auto& lr : L)
       apply_left(lr, lr.U, lr.ldu, local_cols(m, b, lr.r, P), pf, mif, nif, lr.w.Wu_all + plan_.off_u[pf], mif,
@@ -1188,8 +1250,10 @@ void DistFactor::form_uv(int64_t steps, bool final_block, int64_t r0f, int64_t m
   if (final_block)
     for (auto& lr : L) {
       if (int(pf % P) != lr.r) continue;
-      fold_cols(lr, lr.U, m, lr.ldu, pf, nif, lr.w.Usfin);
-      fold_cols(lr, lr.V, n, lr.ldv, pf, nif, lr.w.Vsfin);
+      const int64_t kf = std::min(mif, nif);
+      // fat: X = Vs [D 0] (Q blockdiag(Us, I))^T -- U takes Vs, V takes Us
+      fold_cols(lr, lr.U, m, lr.ldu, pf, kf, final_fat ? lr.w.Vsfin : lr.w.Usfin);
+      fold_cols(lr, lr.V, n, lr.ldv, pf, kf, final_fat ? lr.w.Usfin : lr.w.Vsfin);
     }
   (void)r0f;
 }
@@ -1301,7 +1365,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
                         double* const* V_loc, const int64_t* ldv_loc, randutv_info* info) {
   if (!comm) return -2;
   if (m < 1) return -3;
-  if (n < 1 || n > m) return -4;
+  if (n < 1) return -4;
   if (!A_loc || !lda_loc) return -5;
   if (b < 1 || b > RANDUTV_MAX_B) return -7;
   if (q < 0) return -8;

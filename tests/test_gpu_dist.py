@@ -313,3 +313,31 @@ def test_dist_weak_scaling_shapes_loopback(nranks):
     torch.cuda.synchronize()
     d1 = torch.diagonal(T1).abs().cpu().numpy()
     assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * a)
+
+
+@pytest.mark.parametrize("m,n,b,q,nranks,uv", [(300, 500, 50, 1, 2, True), (400, 1000, 64, 1, 3, False),
+                                               (130, 400, 32, 2, 4, True), (100, 333, 128, 1, 3, True),
+                                               (256, 300, 50, 1, 5, False), (60, 700, 16, 1, 8, True)])
+def test_dist_fat_parity(m, n, b, q, nranks, uv):
+    """Fat inputs m < n (Remark "The case m < n", R8) through the multi-GPU
+    algorithm: the final m_i x n_i block spans several ranks' columns; its
+    transpose is allgathered and QR-factored on every rank, T(I1, J) and V are
+    transformed through an allreduced r0 x m_i product.  T against the oracle's
+    parity rule and the single-GPU fat path; with U, V the exact invariants."""
+    A = testmat.gaussian(m, n, m + 3 * n + nranks)
+    ref = oracle.randutv(A, b, q, 3, build_ortho=False)
+    if uv:
+        U, T, V, info = run_dist_uv(A, nranks, b, q, 3)
+        a = np.linalg.norm(A)
+        assert np.linalg.norm(A - U @ T @ V.T) <= 1e-13 * n * a
+        assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-13 * n
+        assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-13 * n
+    else:
+        T, info = run_dist(A, nranks, b, q, 3)
+    assert info.k_done == m
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+    assert np.all(np.tril(T, -1) == 0.0)
+    _, T1, _, _ = P.randutv(to_dev(A), b, q, 3, with_uv=False)
+    d1, dd = np.abs(np.diag(T1.cpu().numpy())), np.abs(np.diag(T))
+    assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * ref["a_fro"])

@@ -385,6 +385,12 @@ def test_poisoned_workspace_initcheck():
             Ts, _ = D_.factor(comm, sh, 700, 520, 64, 2, 3, oversample=6)
             comm.close()
             out += [D_.assemble(Ts, 520, 64)]
+            A3 = to_dev(testmat.gaussian(300, 640, 4))   # fat: the final block spans the ranks
+            comm = D_.loopback(3)
+            sh = [D_.shard(A3, 64, r, 3) for r in range(3)]
+            Us, Ts, Vs, _ = D_.factor(comm, sh, 300, 640, 64, 1, 5, with_uv=True)
+            comm.close()
+            out += [D_.assemble(Us, 300, 64), D_.assemble(Ts, 640, 64), D_.assemble(Vs, 640, 64)]
             torch.cuda.synchronize()
             runs.append([to_host(x) for x in out])
         finally:
