@@ -924,6 +924,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           qw.flag_count = &nflags_[l];
           qw.flag_cap = lr.w.qflags_cap;
         }
+        qw.orth_tol = kRFactorOrthTol;  // R11 enters T
         int rc = panel_qr(hp, mi, b, Wu, mi, Wu + wun + size_t(b) * b, b, lr.w.tau, Wu + wun, b, qw);
         if (rc != OK) return rc;
         // T(I2,J2) = R11 (replaced by D after the SVD), T(I3,J2) = 0
@@ -1006,6 +1007,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
           QrWork qw = lr.w.qw;
           qw.mode = o.qr_mode;
           qw.fallbacks = &fallbacks;
+          qw.orth_tol = kRFactorOrthTol;
           int rc = panel_qr(st, mi, ni, Wf, mi, lr.w.Rfin, ni, lr.w.tau, lr.w.Tfin, ni, qw);
           if (rc != OK) return rc;
         } else {

@@ -479,7 +479,9 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       copy_matrix(hp, mi, b, X, m, Wu, ldwu);
       double* Tu = w.Tu + size_t(si) * b * b;
       double* R11 = w.Rall + size_t(si) * b * b;
-      check_qr(panel_qr(hp, mi, b, Wu, ldwu, R11, b, w.tau, Tu, b, w.qw));
+      QrWork qwu = w.qw;  // R11 enters T: CholeskyQR2 only while R is backward stable
+      qwu.orth_tol = kRFactorOrthTol;
+      check_qr(panel_qr(hp, mi, b, Wu, ldwu, R11, b, w.tau, Tu, b, qwu));
       // T(I2,J2) = R11 (replaced by D after the batched SVD), T(I3,J2) = 0
       copy_matrix(hp, b, b, R11, b, X, m);
       set_zero(hp, mi - b, b, X + b, m);
@@ -524,7 +526,9 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         double* Wf = uv ? (w.Wu_all + p.off_u[i - 1]) : w.Vu;
         int64_t ldwf = uv ? mi : m;
         copy_matrix(st, mi, ni, X, m, Wf, ldwf);
-        check_qr(panel_qr(st, mi, ni, Wf, ldwf, w.Rfin, ni, w.tau, w.Tu + size_t(p.nrand) * b * b, ni, w.qw));
+        QrWork qwf = w.qw;
+        qwf.orth_tol = kRFactorOrthTol;
+        check_qr(panel_qr(st, mi, ni, Wf, ldwf, w.Rfin, ni, w.tau, w.Tu + size_t(p.nrand) * b * b, ni, qwf));
       } else if (mi < ni) {
         // fat (Remark "The case m < n"): unpivoted QR of the ROWS,
         // X^T = Q [Rf; 0]; with Rf = Ur D Vr^T: X = Vr [D 0] (Q blockdiag(Ur, I))^T
@@ -532,7 +536,9 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         double* Wf = uv ? (w.Wv_all + p.off_v[i - 1]) : w.Wt;
         int64_t ldwf = uv ? ni : n;
         transpose_matrix(st, mi, ni, X, m, Wf, ldwf);
-        check_qr(panel_qr(st, ni, mi, Wf, ldwf, w.Rfin, mi, w.tau, w.Tu + size_t(p.nrand) * b * b, mi, w.qw));
+        QrWork qwf = w.qw;
+        qwf.orth_tol = kRFactorOrthTol;
+        check_qr(panel_qr(st, ni, mi, Wf, ldwf, w.Rfin, mi, w.tau, w.Tu + size_t(p.nrand) * b * b, mi, qwf));
       } else {
         copy_matrix(st, ni, ni, X, m, w.Rfin, ni);
       }
@@ -978,6 +984,7 @@ int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R,
     w.q1_elems = q1;
     w.small = (double*)(((uintptr_t)(w.q1 + q1) + 255) & ~uintptr_t(255));
     w.mode = mode;
+    w.orth_tol = kRFactorOrthTol;  // the caller keeps R
     int fb = 0;
     w.fallbacks = &fb;
     int rc = panel_qr(stream ? (cudaStream_t)stream : cudaStreamPerThread, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);

@@ -95,7 +95,10 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w);
 // ev_fork); the caller must wait for ev_join before using them.
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
                  int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems,
-                 cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr);
+                 cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
+                 double dev_max = 0.5);
+// orth_tol for panels whose R factor is kept (see QrWork::orth_tol)
+constexpr double kRFactorOrthTol = 1e-7;
 // V(0:b, 0:b) <- unit lower L from w.F
 void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double* V, int64_t ldv);
 
@@ -110,6 +113,10 @@ struct QrWork {
   size_t q1_elems = 0;
   double* small = nullptr;  // small_work_elems(b) doubles
   int mode = 0;             // 0: CholeskyQR2 + reconstruction, Householder fallback; 1: Householder only
+  // CholeskyQR2 accepted while max|Q1^T Q1 - I| <= orth_tol: 0.5 where only the
+  // span is used (QR(Y): kappa up to ~1e7); kRFactorOrthTol where R enters T
+  // (column panels, final blocks: kappa <~ 3e4, R backward stable to O(u))
+  double orth_tol = 0.5;
   int* fallbacks = nullptr; // host counter of fallbacks taken (may be null)
   // Optimistic mode (no host synchronisation): the CholeskyQR results are used
   // unconditionally and each decision flag goes to dev_flags[*flag_count]++;

@@ -535,7 +535,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
     cudaStream_t rs = recon_side_stream();
     cudaEvent_t ef = recon_event(0), ej = recon_event(1);
-    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems, rs, ef, ej);
+    small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems, rs, ef, ej, w.orth_tol);
     const bool ok = optimistic || read_flag_sync(st, sw.flag) == 0;
     if (ok) {
       if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1

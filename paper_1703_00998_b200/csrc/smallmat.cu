@@ -800,7 +800,7 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w) {
 
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
                  int64_t ldr, double* tau, double* Tw, int64_t ldt, double* part, size_t part_elems,
-                 cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+                 cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join, double dev_max) {
   ReconArgs a;
   a.d = SmallDims{(int)b, w.bp, w.bp / TS};
   a.W2 = w.W2;
@@ -822,7 +822,7 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
   a.ldt = ldt;
   a.tau = tau;
   a.flag = w.flag;
-  a.dev_max = 0.5;
+  a.dev_max = dev_max;
   const int bp = w.bp;
   {
     ProfScope _p(st, C_QR_SMALL, 0.0);

@@ -398,3 +398,23 @@ def test_poisoned_workspace_initcheck():
     for a, p in zip(*runs):
         assert np.all(np.isfinite(p))
         assert np.array_equal(a, p)
+
+
+@pytest.mark.parametrize("m,n", [(149, 19), (85, 38), (24, 128), (34, 300), (400, 256)])
+def test_final_block_r_factor_accuracy(m, n):
+    """b >= min(m, n): the whole matrix is the final block, whose Householder R
+    factor is kept in T.  With kappa ~ 3e7 (inside CholeskyQR2's range, where
+    its R is no longer backward stable) the panel QR must fall back to
+    Householder (QrWork::orth_tol = kRFactorOrthTol): |diag T| equal to the
+    singular values to O(k eps ||A||) (was ~1e-11 off before the tolerance)."""
+    rng = np.random.default_rng(m * 1000 + n)
+    k = min(m, n)
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    s = np.logspace(0, -7.5, k)
+    A = np.asfortranarray(U @ np.diag(s) @ V.T)
+    _, T, _, info = P.randutv(to_dev(A), 512, 1, 3, with_uv=False)
+    torch.cuda.synchronize()
+    d = np.sort(np.abs(np.diag(to_host(T))[:k]))[::-1]
+    sv = np.linalg.svd(A, compute_uv=False)
+    assert np.abs(d - sv).max() <= 10 * k * EPS * sv[0], np.abs(d - sv).max()

@@ -41,4 +41,13 @@ for _ in range(N):
         ok = False; par = repr(e)
     if not ok:
         fails += 1; print("FAIL", dict(m=m, n=n, b=b, q=q, kind=kind, qm=qm, p=p, ks=ks, uv=uv, seed=seed), par, flush=True)
+        try:  # which side is off: both |diag T| (sorted) against LAPACK's singular values
+            k = min(m, n)
+            if ks == 0 and bb >= k:
+                sv = np.linalg.svd(A, compute_uv=False)
+                dg_ = np.sort(np.abs(np.diag(T)[:k]))[::-1]; do_ = np.sort(np.abs(np.diag(ref["T"])[:k]))[::-1]
+                print("   max|gpu - svd| %.3e  max|oracle - svd| %.3e  sigma_min %.3e  fallbacks %d"
+                      % (np.abs(dg_ - sv).max(), np.abs(do_ - sv).max(), sv.min(), info.qr_fallbacks), flush=True)
+        except Exception as e:  # noqa: BLE001
+            print("   diag:", e)
 print("cases", N, "fails", fails, "time", round(time.time() - t0, 1), flush=True)
