@@ -18,8 +18,14 @@
  *   - Return value (LAPACK ``info`` style): 0 = success; -k = argument k
  *     (1-based, in the order of randutv_factor's parameter list) is invalid;
  *     RANDUTV_ERR_* (> 0) below otherwise.  randutv_strerror() names them.
- *   - The library keeps one cached device workspace per process (grown on
- *     demand, guarded by a mutex); calls from several host threads serialise.
+ *   - The library keeps one cached device workspace (and one staging buffer
+ *     for host-buffer calls) per device, grown on demand.  Host threads
+ *     serialise on a mutex while they enqueue, and on the device every call's
+ *     work is ordered after the previous call's on the same device (the call's
+ *     stream first waits on an event recorded at the end of the previous
+ *     call), so concurrent calls from several threads or streams never share
+ *     the cached workspace at the same time.  Each device's kernel attributes
+ *     are set on first use on that device.
  */
 #ifndef RANDUTV_H
 #define RANDUTV_H
@@ -41,8 +47,8 @@ extern "C" {
 #define RANDUTV_ERR_NONFINITE 1   /* A holds NaN or Inf                */
 #define RANDUTV_ERR_CUDA 2        /* a CUDA runtime error                             */
 #define RANDUTV_ERR_NOMEM 3       /* device allocation failed                         */
-#define RANDUTV_ERR_NCCL 4        /* reserved for the multi-GPU path                  */
-#define RANDUTV_ERR_UNSUPPORTED 5 /* shape outside this build (e.g. > 65536 rows)    */
+#define RANDUTV_ERR_NCCL 4        /* NCCL error, or a collective timed out (multi-GPU) */
+#define RANDUTV_ERR_UNSUPPORTED 5 /* shape outside this build                         */
 
 #define RANDUTV_MAX_B 512
 
@@ -107,11 +113,15 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
                    int64_t k_stop, double* U, double* T, double* V);
 
 /* As randutv_factor, with options and diagnostics.  Device pointers are
- * processed asynchronously on opts->stream, except that the call synchronises
- * that stream once after validating A (non-finite scan), once per step when
- * opts->tol > 0 (early-stop test) and once per panel QR / re-orthonormalisation
- * in qr_mode 0 (the CholeskyQR2 fallback decision).  Returns after all work is enqueued; with
- * host buffers it returns after completion. */
+ * processed on opts->stream.  The host waits on that stream: once after
+ * validating A (non-finite scan); once per randomized step in qr_mode 0 for
+ * the sketch side's CholeskyQR decisions (an event after QR(Y), read while the
+ * P = T W_v GEMM runs); once per step when opts->tol > 0 (early-stop test);
+ * once after the loop for the column panels' CholeskyQR decisions; and once at
+ * the end when info != NULL.  The small SVDs and folds after the loop are
+ * enqueued only, so with info == NULL the call returns before they complete
+ * (synchronise opts->stream before reading T).  With host buffers it returns
+ * after completion. */
 RANDUTV_API int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
                       int32_t q, uint64_t seed, int64_t k_stop, double* U, double* T, double* V,
                       randutv_info* info);

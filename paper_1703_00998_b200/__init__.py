@@ -183,8 +183,10 @@ def _ld(X) -> int:
 
 
 def _stream(stream, device=None):
+    """cudaStream_t of ``stream`` (a torch.cuda.Stream or a raw handle); None:
+    torch's current stream."""
     if stream is not None:
-        return ctypes.c_void_p(int(stream))
+        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
     torch = _torch()
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 

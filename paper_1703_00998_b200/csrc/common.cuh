@@ -3,8 +3,10 @@
 // dimension ld lives at p[i + j * ld].
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 
 namespace rutv {
 
@@ -32,6 +34,47 @@ struct CudaError {
 #define RUTV_LAUNCH_CK() RUTV_CK(cudaGetLastError())
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+  int d = 0;
+  RUTV_CK(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) throw CudaError{cudaErrorInvalidDevice, "device index >= 64"};
+  return d;
+}
+
+// cudaFuncSetAttribute acts on the current device only: run a kernel's
+// attribute setup once per device (bit d of the mask = done on device d).
+struct OncePerDevice {
+  std::atomic<unsigned long long> mask{0};
+  std::mutex mu;
+  template <class F>
+  void operator()(F&& f) {
+    const unsigned long long bit = 1ull << current_device();
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    std::lock_guard<std::mutex> lock(mu);
+    if (mask.load(std::memory_order_relaxed) & bit) return;
+    f();
+    mask.fetch_or(bit, std::memory_order_release);
+  }
+};
+
+// Raise a kernel's dynamic shared-memory limit to >= bytes on the current
+// device (tracked per device; a larger later request raises it again).
+struct SmemAttrPerDevice {
+  std::mutex mu;
+  size_t set[kMaxDevices] = {};
+  template <class K>
+  void ensure(K kern, size_t bytes, bool nonportable_cluster = false) {
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& s = set[current_device()];
+    if (bytes <= s) return;
+    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (nonportable_cluster) RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    s = bytes;
+  }
+};
 
 // Bump allocator over one device workspace block (256-byte aligned slices).
 struct Arena {

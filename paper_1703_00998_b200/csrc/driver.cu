@@ -34,11 +34,43 @@ namespace {
 
 constexpr int kYFlags = 16;  // per-step sketch-side CholeskyQR decision slots (reorthos, QR(Y))
 
+// Host threads serialise on g_mu while they enqueue; on the device, every
+// call's work is ordered after the previous call's on the same device (the
+// cached workspace and the shared side streams / events are reused), see
+// CallOrder.  Cached buffers are kept per device.
 std::mutex g_mu;
-void* g_ws = nullptr;
-size_t g_ws_bytes = 0;
-void* g_stage = nullptr;   // device staging for host-buffer calls
-size_t g_stage_bytes = 0;
+struct DevState {
+  void* ws = nullptr;      // cached workspace (calls without opts.workspace)
+  size_t ws_bytes = 0;
+  void* stage = nullptr;   // device staging for host-buffer calls
+  size_t stage_bytes = 0;
+  cudaEvent_t last = nullptr;  // recorded at the end of the previous call's work
+};
+DevState g_dev[kMaxDevices];
+
+DevState& dev_state() { return g_dev[current_device()]; }
+
+// Scope of one C-ABI call on stream st: st first waits for everything the
+// previous call on this device enqueued (on any stream: all of them are joined
+// into that call's stream before it records `last`), and at scope exit `last`
+// is re-recorded on st.  Two threads, or two user streams, therefore never run
+// on the same cached workspace at once.
+struct CallOrder {
+  cudaStream_t st;
+  explicit CallOrder(cudaStream_t s) : st(s) {
+    DevState& d = dev_state();
+    if (d.last) RUTV_CK(cudaStreamWaitEvent(st, d.last, 0));
+  }
+  ~CallOrder() {
+    DevState& d = dev_state();
+    if (!d.last && cudaEventCreateWithFlags(&d.last, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      d.last = nullptr;
+      return;
+    }
+    if (cudaEventRecord(d.last, st) != cudaSuccess) cudaGetLastError();
+  }
+};
 
 struct Plan {
   int64_t m, n, b;
@@ -689,45 +721,40 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   return RANDUTV_OK;
 }
 
-void* cached_ws(size_t bytes) {
-  if (bytes > g_ws_bytes) {
-    if (g_ws) {
-      cudaDeviceSynchronize();
-      cudaFree(g_ws);
-      g_ws = nullptr;
-      g_ws_bytes = 0;
+// grow-only cached device buffer of the current device (a regrow waits for
+// the device: earlier calls may still use the old block)
+void* cached_buffer(void*& p, size_t& have, size_t bytes) {
+  if (bytes > have) {
+    if (p) {
+      RUTV_CK(cudaDeviceSynchronize());
+      cudaFree(p);
+      p = nullptr;
+      have = 0;
     }
-    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) {
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
       cudaGetLastError();
-      g_ws = nullptr;
+      p = nullptr;
       return nullptr;
     }
-    g_ws_bytes = bytes;
+    have = bytes;
   }
-  if (getenv("RANDUTV_POISON_WORKSPACE")) {  // test hook, see poison_workspace (misc.cu)
+  return p;
+}
+
+void* cached_ws(size_t bytes) {
+  DevState& d = dev_state();
+  void* ws = cached_buffer(d.ws, d.ws_bytes, bytes);
+  if (ws && getenv("RANDUTV_POISON_WORKSPACE")) {  // test hook, see poison_workspace (misc.cu)
     RUTV_CK(cudaDeviceSynchronize());
-    RUTV_CK(cudaMemset(g_ws, 0xFF, g_ws_bytes));
+    RUTV_CK(cudaMemset(ws, 0xFF, d.ws_bytes));
     RUTV_CK(cudaDeviceSynchronize());
   }
-  return g_ws;
+  return ws;
 }
 
 void* cached_stage(size_t bytes) {
-  if (bytes > g_stage_bytes) {
-    if (g_stage) {
-      cudaDeviceSynchronize();
-      cudaFree(g_stage);
-      g_stage = nullptr;
-      g_stage_bytes = 0;
-    }
-    if (cudaMalloc(&g_stage, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      g_stage = nullptr;
-      return nullptr;
-    }
-    g_stage_bytes = bytes;
-  }
-  return g_stage;
+  DevState& d = dev_state();
+  return cached_buffer(d.stage, d.stage_bytes, bytes);
 }
 
 int validate(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, int64_t k_stop, double* U,
@@ -790,6 +817,7 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     const bool host = mem_kind(A) == MEM_HOST || mem_kind(T) == MEM_HOST || (U && mem_kind(U) == MEM_HOST) ||
                       (V && mem_kind(V) == MEM_HOST);
     cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+    CallOrder order(st);
     const size_t need = workspace_bytes(make_plan(m, n, b, q, U != nullptr, o.oversample));
     void* ws = o.workspace;
     size_t wsb = o.workspace_bytes;
@@ -827,13 +855,15 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
                               cudaMemcpyDefault, st));
     // T host buffer pinned: copy T's column blocks back as they become final
     // (after each in-loop fold) on a copy stream, overlapping the rest of the
-    // factorization; the remainder is copied at the end
+    // factorization; the remainder is copied at the end.  Not when T aliases
+    // A (in place): a retry after a failed optimistic CholeskyQR decision
+    // re-stages A, which must then still be the input.
     int64_t copied = 0;
     cudaStream_t cps = nullptr;
     cudaEvent_t cev = nullptr;
     std::function<void(int64_t)> on_final;
     cudaPointerAttributes tat;
-    if (!U && cudaPointerGetAttributes(&tat, T) == cudaSuccess && tat.type == cudaMemoryTypeHost) {
+    if (!U && opt && cudaPointerGetAttributes(&tat, T) == cudaSuccess && tat.type == cudaMemoryTypeHost) {
       cps = side_stream(2);
       RUTV_CK(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming));
       on_final = [&](int64_t cols) {
@@ -953,10 +983,11 @@ int randutv_dgemm(int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t 
   try {
     size_t part = size_t(12) * std::max<int64_t>(M, 1) * std::max<int64_t>(N, 1) + size_t(148) * 32 * 1024;
     part = std::min(part, size_t(1) << 30);
+    cudaStream_t st = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    CallOrder order(st);
     double* ws = (double*)cached_ws(part * sizeof(double));
     if (!ws) return RANDUTV_ERR_NOMEM;
-    dgemm(stream ? (cudaStream_t)stream : cudaStreamPerThread, transa != 0, transb != 0, M, N, K, alpha, A, lda, B,
-          ldb, beta, C, ldc, ws, part);
+    dgemm(st, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, part);
   } catch (const CudaError&) {
     return RANDUTV_ERR_CUDA;
   }
@@ -977,6 +1008,8 @@ int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R,
     size_t part = size_t(12) * m * b + size_t(148) * 32 * 1024;
     size_t extra = size_t(3) * 32 * b + 1024;
     size_t q1 = size_t(m) * b, sm = small_work_elems(b) + 64;
+    cudaStream_t st = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    CallOrder order(st);
     double* ws = (double*)cached_ws((part + extra + q1 + sm) * sizeof(double));
     if (!ws) return RANDUTV_ERR_NOMEM;
     QrWork w{ws, part, ws + part, ws + part + 32 * b, ws + part + 64 * b};
@@ -987,7 +1020,7 @@ int randutv_panel_qr_ex(int64_t m, int64_t b, double* V, int64_t ldv, double* R,
     w.orth_tol = kRFactorOrthTol;  // the caller keeps R
     int fb = 0;
     w.fallbacks = &fb;
-    int rc = panel_qr(stream ? (cudaStream_t)stream : cudaStreamPerThread, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
+    int rc = panel_qr(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
     if (fallback) *fallback = fb;
     return rc;
   } catch (const CudaError&) {
@@ -1022,6 +1055,7 @@ int randutv_rsvd(const randutv_opts* opts, int64_t m, int64_t n, const double* A
   std::lock_guard<std::mutex> lock(g_mu);
   try {
     cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+    CallOrder order(st);
     const int64_t mx = std::max(m, n);
     Arena ar;
     ar.dry = true;
@@ -1082,7 +1116,9 @@ int randutv_rsvd(const randutv_opts* opts, int64_t m, int64_t n, const double* A
     set_gemm_role(C_GEMM_OTHER);
     dgq(false, false, m, bs, n, A, lda, Y2, n, G, m);                   // B = A Q
     set_gemm_role(C_GEMM_QR);
-    rc = panel_qr(st, m, bs, G, m, R, bs, tau, Tw, bs, qw);             // B = Q_B R_B
+    QrWork qwb = qw;  // R_B feeds the SVD: CholeskyQR2 only while R is backward stable (R20)
+    qwb.orth_tol = kRFactorOrthTol;
+    rc = panel_qr(st, m, bs, G, m, R, bs, tau, Tw, bs, qwb);            // B = Q_B R_B
     if (rc != OK) return rc;
     thin_q(st, m, bs, G, m, Tw, bs, Z, m, tmp, qw.part, qw.part_elems);
     jacobi_svd_batched(st, 1, (int)bs, R, bs, bs * bs, Dall, Us, Vs, jw, nullptr);  // R_B = Us D Vs^T
@@ -1107,10 +1143,11 @@ int randutv_small_svd_batched(int32_t batch, int32_t k, const double* R, int64_t
   std::lock_guard<std::mutex> lock(g_mu);
   try {
     size_t need = jacobi_work_elems(batch, k);
+    cudaStream_t st = stream ? (cudaStream_t)stream : cudaStreamPerThread;
+    CallOrder order(st);
     double* ws = (double*)cached_ws(need * sizeof(double));
     if (!ws) return RANDUTV_ERR_NOMEM;
-    jacobi_svd_batched(stream ? (cudaStream_t)stream : cudaStreamPerThread, batch, k, R, ldr, strideR, D, Us, Vs,
-                       ws, sweeps);
+    jacobi_svd_batched(st, batch, k, R, ldr, strideR, D, Us, Vs, ws, sweeps);
   } catch (const CudaError&) {
     return RANDUTV_ERR_CUDA;
   }

@@ -640,12 +640,9 @@ void launch_c2(cudaStream_t st, int batch, int k, double* Bw, double* Wm, int* c
   const int epl = k <= 64 ? 2 : (k <= 128 ? 4 : 8);
   const size_t smem2 = size_t(2) * 2 * 16 * 32 * epl * sizeof(double);
   auto kern = epl == 2 ? jacobi_cluster2_k<2> : (epl == 4 ? jacobi_cluster2_k<4> : jacobi_cluster2_k<8>);
-  static bool attr2[3] = {false, false, false};
+  static OncePerDevice attr2[3];
   const int ai = epl == 2 ? 0 : (epl == 4 ? 1 : 2);
-  if (!attr2[ai]) {
-    RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    attr2[ai] = true;
-  }
+  attr2[ai]([&] { RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2)); });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(csize, batch, 1);
   cfg.blockDim = dim3(JNT, 1, 1);
@@ -690,11 +687,8 @@ void launch_finalize(cudaStream_t st, int batch, int k, const JacobiBufs& jb, do
   double* Wm = jb.Wm;
   int* counts = jb.counts;
   const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
-  static size_t attr_f = 0;
-  if (fsmem > 48 * 1024 && fsmem > attr_f) {
-    RUTV_CK(cudaFuncSetAttribute(jacobi_finalize_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-    attr_f = fsmem;
-  }
+  static SmemAttrPerDevice attr_f;
+  if (fsmem > 48 * 1024) attr_f.ensure(jacobi_finalize_k, fsmem);
   { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out); }
   RUTV_LAUNCH_CK();
 }
@@ -739,12 +733,8 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
   } else if (k > 1 && csize <= MAX_CLUSTER) {
 
     // one cluster per matrix runs every round and sweep in-kernel
-    static size_t attr_c = 0;
-    if (smem > attr_c) {
-      RUTV_CK(cudaFuncSetAttribute(jacobi_cluster_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      RUTV_CK(cudaFuncSetAttribute(jacobi_cluster_k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_c = smem;
-    }
+    static SmemAttrPerDevice attr_c;
+    attr_c.ensure(jacobi_cluster_k, smem, true);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize, batch, 1);
     cfg.blockDim = dim3(32 * d.kb, 1, 1);  // one warp per column pair of a block pair
@@ -761,11 +751,8 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
     count_launch(K_SVD);
     RUTV_CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_k, d, Bw, Wm, counts, tol));
   } else if (k > 1) {
-    static size_t attr_smem = 0;
-    if (smem > 48 * 1024 && smem > attr_smem) {
-      RUTV_CK(cudaFuncSetAttribute(jacobi_round_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_smem = smem;
-    }
+    static SmemAttrPerDevice attr_r;
+    if (smem > 48 * 1024) attr_r.ensure(jacobi_round_k, smem);
     // Sweeps are launched in chunks; between chunks the host reads the
     // per-matrix rotation counts once (one sync) and stops when all converged.
     int sweep = 0;

@@ -329,13 +329,12 @@ leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ld
 template <int W, int RPT>
 void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* V, int64_t ldv, double* R,
                  int64_t ldr, double* tau, double* Tw, int64_t ldt) {
-  static bool attr = false;
+  static OncePerDevice attr;
   auto kern = leaf_qr_kernel<W, RPT>;
-  if (!attr) {
+  attr([&] {
     RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaf_smem_bytes<W, RPT>()));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(QR_NT, 1, 1);
@@ -430,8 +429,12 @@ int qr_max_rows() { return QR_MAX_CLUSTER * QR_NT * 16; }
 size_t qr_work_elems(int64_t b) { return size_t(3) * 32 * size_t(b) + 1024; }
 
 namespace {
+int panel_qr_tsqr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                  double* Tw, int64_t ldt, const QrWork& w);
+
 int panel_qr_hh(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
                 double* Tw, int64_t ldt, const QrWork& w) {
+  if (m > qr_max_rows()) return panel_qr_tsqr(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
   GemmRole role(C_GEMM_QR);
   int W, RPT;
   const int64_t cap = int64_t(QR_MAX_CLUSTER) * QR_NT;
@@ -473,6 +476,65 @@ int panel_qr_hh(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, d
     if (j0 > 0)    // Tw[0:j0, j0:j0+wj] = -Tw[0:j0, 0:j0] O(:, 0:j0)^T
       dgemm(st, false, true, j0, wj, j0, -1.0, Tw, ldt, w.sfull, wj, 0.0, Tw + j0 * ldt, ldt, w.part, w.part_elems);
   }
+  return OK;
+}
+
+int read_flag_sync(cudaStream_t st, const int* dflag);
+
+// Householder QR of a panel taller than the cluster leaf kernel holds
+// (m > qr_max_rows()): TSQR + Householder reconstruction (Ballard et al. 2015,
+// the TSQR-HR variant; the same reconstruction as the CholeskyQR2 path, R20).
+//   1. row chunks of h <= 8192 rows: Householder QR each (leaf kernel), keep
+//      R_i stacked in S (nc b x b) and the chunk's thin Q_i (into w.q1);
+//   2. Householder QR of the stack S = Q_s R, thin Q_s;
+//   3. Q = blockdiag(Q_i) Q_s (m x b, orthonormal to rounding whatever the
+//      rank or conditioning of the panel);
+//   4. the reconstruction with Q as "Q1" and R as "R1" (G2 = Q^T Q = I to
+//      rounding, so its second pass is the first-order closed form): W, T_w,
+//      tau and R_h = S R -- in exact arithmetic exactly the reflectors of the
+//      column-by-column Householder QR (R3).
+// Needs w.q1 (m x b) and w.small; stack height nc b <= qr_max_rows().
+int panel_qr_tsqr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
+                  double* Tw, int64_t ldt, const QrWork& w) {
+  if (!w.q1 || !w.small || size_t(m) * b > w.q1_elems || b > 512) return ERR_UNSUPPORTED;
+  constexpr int64_t kChunk = 8192;
+  const int64_t nc = cdiv(m, kChunk);
+  const int64_t h = cdiv(m, nc);     // balanced chunks of h or h - 1 >= b rows
+  const int64_t hs = nc * b;         // stack height
+  if (hs > qr_max_rows() || h - 1 < b) return ERR_UNSUPPORTED;
+  const size_t stack = size_t(hs) * b;
+  if (w.part_elems < 2 * stack + (size_t(1) << 20)) return ERR_UNSUPPORTED;
+  GemmRole role(C_GEMM_QR);
+  QrWork ws = w;                     // the stack S and Q_s at the tail of the split-K scratch
+  ws.part_elems = w.part_elems - 2 * stack;
+  double* S = w.part + ws.part_elems;
+  double* Qs = S + stack;
+  SmallWork sw = carve_small(w.small, b);
+  const int bp = sw.bp;
+  double* tmp = sw.W1;               // b x b scratch (the Gram slot is unused on this path)
+  for (int64_t i = 0; i < nc; ++i) { // 1. chunk QRs, R_i -> S(i b : i b + b, :)
+    const int64_t r0 = i * h, hi = std::min(h, m - r0);
+    int rc = panel_qr_hh(st, hi, b, V + r0, ldv, S + i * b, hs, tau, Tw, ldt, ws);
+    if (rc != OK) return rc;
+    thin_q(st, hi, b, V + r0, ldv, Tw, ldt, w.q1 + r0, m, tmp, ws.part, ws.part_elems);
+  }
+  int rc = panel_qr_hh(st, hs, b, S, hs, R, ldr, tau, Tw, ldt, ws);  // 2. S = Q_s R
+  if (rc != OK) return rc;
+  thin_q(st, hs, b, S, hs, Tw, ldt, Qs, hs, tmp, ws.part, ws.part_elems);
+  for (int64_t i = 0; i < nc; ++i) { // 3. Q = blockdiag(Q_i) Q_s -> V, then -> q1
+    const int64_t r0 = i * h, hi = std::min(h, m - r0);
+    dgemm(st, false, false, hi, b, b, 1.0, w.q1 + r0, m, Qs + i * b, hs, 0.0, V + r0, ldv, ws.part, ws.part_elems);
+  }
+  copy_matrix(st, m, b, V, ldv, w.q1, m);
+  // 4. reconstruction: R1 := R (identity-padded), no first-pass breakdown
+  set_identity(st, bp, bp, sw.R1, bp);
+  copy_matrix(st, b, b, R, ldr, sw.R1, bp);
+  RUTV_CK(cudaMemsetAsync(sw.stats, 0, sizeof(double), st));
+  dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, ws.part, ws.part_elems, 0, false, true);
+  small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, ws.part, ws.part_elems, nullptr, nullptr, nullptr, 0.5);
+  if (read_flag_sync(st, sw.flag) != 0) return ERR_UNSUPPORTED;  // Q not orthonormal: cannot happen short of NaN
+  dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, ws.part, ws.part_elems, 0, true);
+  small_put_unit_lower(st, b, sw, V, ldv);
   return OK;
 }
 

@@ -737,13 +737,14 @@ template <class K, class... Args>
 void launch_cluster(K kern, cudaStream_t st, int C, Args... args) {
   // one attribute call per kernel (several kernels share the type K)
   static std::mutex mu;
-  static std::vector<const void*> done;
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
   const size_t smem = sizeof(SmallSm);
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (std::find(done.begin(), done.end(), (const void*)kern) == done.end()) {
+    const std::pair<const void*, int> key((const void*)kern, current_device());
+    if (std::find(done.begin(), done.end(), key) == done.end()) {
       RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      done.push_back((const void*)kern);
+      done.push_back(key);
     }
   }
   cudaLaunchConfig_t cfg = {};

@@ -98,36 +98,90 @@ class Case:
 SEEDS = {"c1": 0, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
 
 
-def config(name: str, scale: float = 1.0, q: int | None = None) -> Case:
+def config(name: str, scale: float = 1.0, q: int | None = None, build_A: bool = True) -> Case:
     """BASELINE.json config ``name`` ('c1'..'c5'); ``scale`` < 1 shrinks it
-    (n -> round(n*scale), b kept unless it would exceed n/4)."""
+    (n -> round(n*scale), b kept unless it would exceed n/4).  ``build_A`` =
+    False returns the parameters only (A = None)."""
     seed = SEEDS[name]
+    mk = (lambda f, *a: f(*a)) if build_A else (lambda f, *a: None)
     if name == "c1":
         n = max(8, round(500 * scale))
         b = min(50, max(2, n // 4))
-        return Case("c1", gaussian(n, n, seed), b, 1 if q is None else q, seed)
+        return Case("c1", mk(gaussian, n, n, seed), b, 1 if q is None else q, seed)
     if name == "c2":
         n = max(8, round(3000 * scale))
         b = min(128, max(2, n // 4))
         s = sigma_exponential(n)
-        return Case("c2", with_spectrum(n, n, s, seed), b, 2 if q is None else q, seed, sigma=s)
+        return Case("c2", mk(with_spectrum, n, n, s, seed), b, 2 if q is None else q, seed, sigma=s)
     if name == "c3":
         n = max(16, round(10000 * scale))
         b = min(256, max(2, n // 8))
         s = sigma_s_shape(n, round(0.2 * n), round(0.3 * n))
-        return Case("c3", with_spectrum(n, n, s, seed), b, 2 if q is None else q, seed, sigma=s)
+        return Case("c3", mk(with_spectrum, n, n, s, seed), b, 2 if q is None else q, seed, sigma=s)
     if name == "c4":
         m, n = max(16, round(20000 * scale)), max(8, round(8000 * scale))
         b = min(256, max(2, n // 8))
-        return Case("c4", gaussian(m, n, seed), b, 1 if q is None else q, seed)
+        return Case("c4", mk(gaussian, m, n, seed), b, 1 if q is None else q, seed)
     if name == "c5":
         n = max(32, round(30000 * scale))
         rank = max(2, round(2000 * scale))
         b = min(512, max(2, n // 16))
         k_stop = max(b, round(2048 * scale))
-        return Case("c5", low_rank_plus_noise(n, rank, 1e-8, seed), b, 1 if q is None else q, seed,
+        return Case("c5", mk(low_rank_plus_noise, n, rank, 1e-8, seed), b, 1 if q is None else q, seed,
                     k_stop=k_stop, tol=1e-6, meta={"rank": rank})
     raise KeyError(name)
+
+
+# --------------------------------------------------------------------------- pinned host inputs
+# OpenBLAS results depend on the kernel family it picks for the CPU and on its
+# thread count (both change the summation order of dgemm / dgeqrf).  The
+# recipes that go through LAPACK/BLAS (c2, c3: Haar QRs and the product; c5:
+# X Y^T) are therefore run in a child process with both pinned, so the bytes
+# of A are the same on every x86-64 host with AVX2 -- the full-size golden
+# oracle values in tests/golden/ are keyed by the SHA-256 of those bytes.
+PINNED_BLAS_ENV = {"OPENBLAS_CORETYPE": "Haswell", "OPENBLAS_NUM_THREADS": "8", "OMP_NUM_THREADS": "8"}
+
+
+def sha256_colmajor(A: np.ndarray) -> str:
+    import hashlib
+    return hashlib.sha256(np.asfortranarray(A).tobytes(order="F")).hexdigest()
+
+
+def config_pinned(name: str, scale: float = 1.0, q: int | None = None, tmpdir: str | None = None) -> Case:
+    """:func:`config` with A built in a child process under ``PINNED_BLAS_ENV``
+    (bit-reproducible across hosts); ``case.meta['sha256']`` = SHA-256 of A's
+    column-major bytes."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    import shutil
+
+    c = config(name, scale, q, build_A=False)
+    if name == "c4":
+        need = 8.8 * max(16, round(20000 * scale)) * max(8, round(8000 * scale))
+    else:
+        need = 8.8 * max(16, round({"c1": 500, "c2": 3000, "c3": 10000, "c5": 30000}[name] * scale)) ** 2
+    d = tmpdir
+    if d is None:  # /dev/shm when it has room (container defaults can be 64 MB), else the temp dir
+        d = "/dev/shm" if os.path.isdir("/dev/shm") and shutil.disk_usage("/dev/shm").free > need else None
+    fd, path = tempfile.mkstemp(suffix=".f64", dir=d)
+    os.close(fd)
+    try:
+        here = os.path.dirname(os.path.abspath(__file__))
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); import testmat; "
+                "c = testmat.config(%r, %r, build_A=True); "
+                "np.asfortranarray(c.A).T.tofile(%r); print(c.A.shape[0], c.A.shape[1])" % (here, name, scale, path))
+        env = dict(os.environ, **PINNED_BLAS_ENV)
+        out = subprocess.run([sys.executable, "-c", code], env=env, check=True, capture_output=True, text=True)
+        m, n = (int(v) for v in out.stdout.split())
+        A = np.fromfile(path, dtype=np.float64).reshape(n, m).T   # column-major m x n, no copy
+    finally:
+        os.unlink(path)
+    c.A = A
+    c.meta["sha256"] = sha256_colmajor(A)
+    return c
 
 
 # --------------------------------------------------------------------------- device generators
