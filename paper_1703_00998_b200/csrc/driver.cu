@@ -105,6 +105,9 @@ Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv, int64_t ovs = 0)
 
 struct Work {
   double *G, *Y, *Y2, *P, *P2, *Vu, *Wt, *Wt2, *tau, *Rtmp, *Ttmp;
+  double *WG, *H;  // look-ahead sketch: [W_u | G'] (m x (b + bs)), H = W_u^T G' (b x bs)
+  double *Pbig, *part2;  // P_big = T(:, J3) Q1(b:, :) (m x b) and its split-K scratch (side stream)
+  size_t part2_elems;
   double *Qo, *Ro, *Do, *Uso, *Vso, *jworko;  // over-sampling: thin Q, R, SVD of R (width b + p)
   double *Tv, *Tu, *Rall, *Dall, *Usall, *Vsall, *jwork;
   double *Rfin, *Dfin, *Usfin, *Vsfin, *jworkf;
@@ -124,8 +127,13 @@ Work carve(Arena& ar, const Plan& p) {
   const int64_t sb = std::max<int64_t>(p.nrand, 1);
   const int64_t bs = b + p.ovs;  // sketch width
   w.G = ar.take<double>(size_t(m) * bs);
-  w.Y = ar.take<double>(size_t(n) * bs);
+  // [Wt | Y] contiguous (ld n): the fused left-apply / next-sketch GEMM
+  // C^T [W_u | G'] writes C^T W_u into Wt and C^T G' into Y in one launch
+  w.Wt = ar.take<double>(size_t(n) * (b + bs));
+  w.Y = w.Wt + size_t(n) * b;
   w.Y2 = ar.take<double>(size_t(n) * bs);
+  w.WG = ar.take<double>(size_t(m) * (b + bs));
+  w.H = ar.take<double>(size_t(b) * bs);
   if (p.ovs > 0) {
     w.Qo = ar.take<double>(size_t(n) * bs);
     w.Ro = ar.take<double>(size_t(bs) * bs);
@@ -136,8 +144,10 @@ Work carve(Arena& ar, const Plan& p) {
   }
   w.P = ar.take<double>(size_t(m) * b);
   w.P2 = ar.take<double>(size_t(m) * b);
-  w.Vu = ar.take<double>(size_t(m) * b);
-  w.Wt = ar.take<double>(size_t(n) * b);
+  w.Pbig = ar.take<double>(size_t(m) * b);
+  w.part2_elems = size_t(8) * m * b + size_t(148) * 32 * 1024;
+  w.part2 = ar.take<double>(w.part2_elems);
+  w.Vu = w.WG;  // W_u (T-only mode) in the first b columns of [W_u | G']
   w.Wt2 = ar.take<double>(size_t(n) * b);
   w.tau = ar.take<double>(size_t(bs));
   w.Rtmp = ar.take<double>(size_t(bs) * bs);
@@ -241,8 +251,26 @@ cudaStream_t priority_stream() {
   return streams[dev];
 }
 
+// The factorization's critical path runs on an internal stream one priority
+// level above the default (joined to the caller's stream at entry and exit):
+// its kernels -- the latency-bound CholeskyQR chains in particular -- are then
+// scheduled ahead of the default-priority side streams' GEMM CTAs they
+// overlap (the look-ahead left update), and behind the panel QR's.
+cudaStream_t crit_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  RUTV_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int least = 0, greatest = 0;
+    RUTV_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RUTV_CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, std::max(greatest, least - 1)));
+  }
+  return streams[dev];
+}
+
 cudaEvent_t overlap_event(int which) {
-  static cudaEvent_t evs[6][64] = {};
+  static cudaEvent_t evs[12][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
@@ -263,7 +291,20 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
                   uint64_t seed, int64_t k_stop, double* U, double* T, double* V, randutv_info* info,
                   void* ws, size_t ws_bytes, bool optimistic,
                   const std::function<void(int64_t)>& on_final = std::function<void(int64_t)>()) {
-  cudaStream_t st = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;
+  cudaStream_t ust = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;  // the caller's stream
+  cudaStream_t st = crit_stream();
+  {
+    cudaEvent_t e = overlap_event(8);
+    RUTV_CK(cudaEventRecord(e, ust));
+    RUTV_CK(cudaStreamWaitEvent(st, e, 0));
+  }
+  struct Join {  // every exit: the caller's stream waits for the internal one
+    cudaStream_t ust, st;
+    ~Join() {
+      cudaEvent_t e = overlap_event(9);
+      if (cudaEventRecord(e, st) != cudaSuccess || cudaStreamWaitEvent(ust, e, 0) != cudaSuccess) cudaGetLastError();
+    }
+  } join_guard{ust, st};
   const bool uv = (U != nullptr);
   const bool reortho = (o.no_reortho == 0);
   Plan p = make_plan(m, n, b, q, uv, o.oversample);
@@ -406,6 +447,26 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   int64_t r0f = 0, nif = 0, mif = 0;
   double trailing = 0.0;
   bool stopped = false;
+  // Look-ahead sketch.  With C = T(r0:m, J3) after the right apply, the next
+  // step's trailing matrix is X' = rows b: of C - W_u Z', Z' = T_u^T W_u^T C
+  // (the left apply), so its first sketch product is
+  //   X'^T G_{i+1} = (U^T C)^T G' = C^T G'',  G' = [0_b; G_{i+1}],
+  //   G'' = U G' = G' - W_u T_u (W_u^T G')
+  // (the same product in exact arithmetic; G'' is formed beside the panel QR,
+  // off the critical path): C^T W_u and X'^T G_{i+1} come out of ONE GEMM,
+  // C^T [W_u | G''] (C read once), the left update is C -= (W_u T_u^T)(C^T W_u)^T, and the next
+  // step's first re-orthonormalisation (or QR(Y) when q = 0) -- a latency-bound
+  // chain -- runs on the critical stream while the left update C -= W_u Z'
+  // runs on a side stream.  The next step waits for that update (ensure_lu)
+  // before anything reads X.
+  bool have_y0 = false;      // w.Y holds this step's X^T G from the look-ahead
+  bool pending_lu = false;   // a look-ahead left update is in flight on side_stream(1)
+  cudaEvent_t lu_join = overlap_event(7);
+  auto ensure_lu = [&]() {
+    if (!pending_lu) return;
+    RUTV_CK(cudaStreamWaitEvent(st, lu_join, 0));
+    pending_lu = false;
+  };
 
   for (int64_t i = 1; i <= p.s; ++i) {
     const int64_t r0 = b * (i - 1);
@@ -419,22 +480,29 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       int64_t ldwv = n;
       double* Tv = w.Tv + size_t(si) * b * b;
       double* TJ = T + r0 * m;
+      cudaStream_t upd = side_stream(1);  // side GEMMs: trailing right update, look-ahead left update, P_big
       // sketch, QR(Y) and P = T W_v, P2 = P T_v: reads T only
-      auto sketch_qr_p = [&](const QrWork& qwy, bool copy_flags) {
+      auto sketch_qr_p = [&](const QrWork& qwy, bool copy_flags, bool use_y0) {
         // ---- sketch
         set_gemm_role(C_GEMM_SKETCH);
         const int64_t p_i = std::min<int64_t>(p.ovs, ni - b);  // over-sampling (R23); 0 = Fig. fig:randUTV
         const int64_t bw = b + p_i;                            // sketch width
-        gaussian_fill(st, w.G, m, mi, bw, seed, uint32_t(i - 1), 0u);
-        dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
+        if (!use_y0) {
+          ensure_lu();
+          gaussian_fill(st, w.G, m, mi, bw, seed, uint32_t(i - 1), 0u);
+          dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, w.Y, n);
+        }
         double* Ycur = w.Y;
         double* Yalt = w.Y2;
         for (int it = 0; it < q; ++it) {
           if (reortho) {
-            svd_sweep_here();
+            // not beside the first chain of a look-ahead step: the left update
+            // GEMM of the previous step fills the SMs there
+            if (!(use_y0 && it == 0)) svd_sweep_here();
             check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, qwy));
             std::swap(Ycur, Yalt);
           }
+          ensure_lu();
           dg(w, st, false, false, mi, bw, ni, 1.0, X, m, Ycur, n, 0.0, w.G, m);      // Z = X Y
           dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);       // Y = X^T Z
         }
@@ -458,14 +526,46 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
           copy_matrix(st, ni, b, Ycur, n, Wv, ldwv);
         }
         svd_sweep_here();
-        check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
-        if (copy_flags && *qwy.flag_count > 0) {
-          RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
-          RUTV_CK(cudaEventRecord(ev_yflags, st));
+        // ---- right apply to all m rows: P = T W_v, P2 = P T_v.
+        // Optimistic CholeskyQR2 path: W_v = [L; -Q1(b:, :) M] (R20), so
+        //   P = T(:, J2) L - (T(:, J3) Q1(b:, :)) M
+        // and the big product P_big = T(:, J3) Q1(b:, :) needs only the first
+        // CholeskyQR pass: it runs on the side stream (after the previous
+        // step's look-ahead left update, stream order) while the second pass
+        // and the reconstruction's latency-bound LU run here.
+        const bool split = copy_flags && panel_qr_begin(st, ni, b, Wv, ldwv, qwy);
+        if (split) {
+          cudaEvent_t f = overlap_event(10), j = overlap_event(11);
+          RUTV_CK(cudaEventRecord(f, st));
+          RUTV_CK(cudaStreamWaitEvent(upd, f, 0));
+          {
+            GemmRole role(C_GEMM_RIGHT);
+            dgemm(upd, false, false, m, b, ni - b, 1.0, TJ + b * m, m, qwy.q1 + b, ni, 0.0, w.Pbig, m, w.part2,
+                  w.part2_elems);
+          }
+          RUTV_CK(cudaEventRecord(j, upd));
+          panel_qr_finish(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy);
+          if (*qwy.flag_count > 0) {
+            RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
+            RUTV_CK(cudaEventRecord(ev_yflags, st));
+          }
+          set_gemm_role(C_GEMM_RIGHT);
+          ensure_lu();
+          dg(w, st, false, false, m, b, b, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);           // T(:, J2) L
+          RUTV_CK(cudaStreamWaitEvent(st, j, 0));
+          int64_t ldm = 0;
+          const double* M = panel_qr_M(qwy, b, &ldm);
+          dg(w, st, false, false, m, b, b, -1.0, w.Pbig, m, M, ldm, 1.0, w.P, m);       // - P_big M
+        } else {
+          check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
+          if (copy_flags && *qwy.flag_count > 0) {
+            RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
+            RUTV_CK(cudaEventRecord(ev_yflags, st));
+          }
+          set_gemm_role(C_GEMM_RIGHT);
+          ensure_lu();
+          dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
         }
-        // ---- right apply to all m rows: P = T W_v, P2 = P T_v
-        set_gemm_role(C_GEMM_RIGHT);
-        dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
         dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
       };
       if (opt_y) {
@@ -474,23 +574,26 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         qwy.dev_flags = w.qflags + w.qflags_cap;  // the kYFlags slots after the panel-QR ones
         qwy.flag_count = &ny;
         qwy.flag_cap = kYFlags;
-        sketch_qr_p(qwy, true);
+        sketch_qr_p(qwy, true, have_y0);
         bool failed = false;
         if (ny > 0) {  // read while the P GEMM runs
           RUTV_CK(cudaEventSynchronize(ev_yflags));
           for (int f = 0; f < ny; ++f) failed |= h_yflags[f] != 0;
         }
-        if (failed) sketch_qr_p(qw_sync, false);
+        if (failed) sketch_qr_p(qw_sync, false, false);  // from scratch: Y = X^T G directly
       } else {
-        sketch_qr_p(qw_sync, false);
+        sketch_qr_p(qw_sync, false, have_y0);
       }
+      have_y0 = false;
+      // the next step is randomized (and not cut by k_stop): look ahead
+      const bool la_next = (b * (i + 1) < m && b * (i + 1) < n) && !(k_stop > 0 && b * i >= k_stop);
+      const int64_t bw_next = la_next ? b + std::min<int64_t>(p.ovs, ni - 2 * b) : 0;
       // The panel QR below reads only the panel block T(r0:m, J2): update it
       // first on the main stream; the rest of the rank-b update (columns J3 and
       // the rows above the panel) runs on a low-priority side stream
       // concurrently with the latency-bound panel QR, and the left apply waits
       // for it.  Side GEMMs are unsplit (no shared split-K scratch).
       dg(w, st, false, true, mi, b, b, -1.0, w.P2 + r0, m, Wv, ldwv, 1.0, X, m);
-      cudaStream_t upd = side_stream(1);
       cudaEvent_t fork = overlap_event(0), join = overlap_event(1);
       RUTV_CK(cudaEventRecord(fork, st));
       RUTV_CK(cudaStreamWaitEvent(upd, fork, 0));
@@ -508,6 +611,13 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       cudaEvent_t fork2 = overlap_event(2), join2 = overlap_event(3);
       RUTV_CK(cudaEventRecord(fork2, st));
       RUTV_CK(cudaStreamWaitEvent(hp, fork2, 0));
+      // late steps: the trailing update (~2 m (n_i - b) b flops) is shorter than
+      // the latency-bound panel QR, SMs idle there -- one more Jacobi sweep
+      if (2.0 * double(m) * double(ni - b) * double(b) < 0.4e-3 * 30e12) svd_sweep_here();
+      if (la_next) {  // G' = [0_b; G_{i+1}] next to W_u (Philox draw of step i+1)
+        gaussian_fill(hp, w.WG + size_t(b) * m + b, m, mi - b, bw_next, seed, uint32_t(i), 0u);
+        set_zero(hp, b, bw_next, w.WG + size_t(b) * m, m);
+      }
       copy_matrix(hp, mi, b, X, m, Wu, ldwu);
       double* Tu = w.Tu + size_t(si) * b * b;
       double* R11 = w.Rall + size_t(si) * b * b;
@@ -517,16 +627,48 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       // T(I2,J2) = R11 (replaced by D after the batched SVD), T(I3,J2) = 0
       copy_matrix(hp, b, b, R11, b, X, m);
       set_zero(hp, mi - b, b, X + b, m);
+      if (la_next) {
+        // G'' = U G' = G' - W_u (T_u (W_u^T G')), so that C^T G'' = (U^T C)^T G'
+        // = X'^T G_{i+1}; and WT = W_u T_u^T for the left update C -= WT (C^T W_u)^T.
+        // G'' is formed here beside the trailing update, WT on the side stream.
+        if (Wu != w.WG) copy_matrix(hp, mi, b, Wu, ldwu, w.WG, m);
+        GemmRole role(C_GEMM_SKETCH);
+        double* Gp = w.WG + size_t(b) * m;
+        dg(w, hp, true, false, b, bw_next, mi, 1.0, w.WG, m, Gp, m, 0.0, w.H, b);        // H = W_u^T G'
+        dg(w, hp, false, false, b, bw_next, b, 1.0, Tu, b, w.H, b, 0.0, w.Rtmp, b);     // T_u H
+        dg(w, hp, false, false, mi, bw_next, b, -1.0, w.WG, m, w.Rtmp, b, 1.0, Gp, m);  // G'' = G' - W_u (T_u H)
+      }
       RUTV_CK(cudaEventRecord(join2, hp));
       RUTV_CK(cudaStreamWaitEvent(st, join2, 0));
+      if (la_next) {  // WT = W_u T_u^T for the left update, on the side stream (after its right update)
+        RUTV_CK(cudaStreamWaitEvent(upd, join2, 0));
+        GemmRole role(C_GEMM_LEFT);
+        dgemm(upd, false, true, mi, b, b, 1.0, w.WG, m, Tu, b, 0.0, w.Pbig, m, nullptr, 0);
+      }
       // ---- left apply to T(r0:m, J3), after the overlapped update
       RUTV_CK(cudaStreamWaitEvent(st, join, 0));
       set_gemm_role(C_GEMM_LEFT);
       const int64_t nc = n - f2;
       double* Cm = T + r0 + f2 * m;
-      dg(w, st, true, false, nc, b, mi, 1.0, Cm, m, Wu, ldwu, 0.0, w.Wt, n);       // C^T W_u
-      dg(w, st, false, false, nc, b, b, 1.0, w.Wt, n, Tu, b, 0.0, w.Wt2, n);        // (C^T W_u) T_u
-      dg(w, st, false, true, mi, nc, b, -1.0, Wu, ldwu, w.Wt2, n, 1.0, Cm, m);      // C -= W_u (.)^T
+      if (la_next) {
+        // [C^T W_u | C^T G''] -> [Wt | Y]: Y = X'^T G_{i+1}, the next step's first sketch product
+        dg(w, st, true, false, nc, b + bw_next, mi, 1.0, Cm, m, w.WG, m, 0.0, w.Wt, n);
+        // C -= (W_u T_u^T)(C^T W_u)^T on the side stream, concurrent with the next step's first chain
+        cudaEvent_t lf = overlap_event(6);
+        RUTV_CK(cudaEventRecord(lf, st));
+        RUTV_CK(cudaStreamWaitEvent(upd, lf, 0));
+        {
+          GemmRole role(C_GEMM_LEFT);
+          dgemm(upd, false, true, mi, nc, b, -1.0, w.Pbig, m, w.Wt, n, 1.0, Cm, m, nullptr, 0);
+        }
+        RUTV_CK(cudaEventRecord(lu_join, upd));
+        pending_lu = true;
+        have_y0 = true;
+      } else {
+        dg(w, st, true, false, nc, b, mi, 1.0, Cm, m, Wu, ldwu, 0.0, w.Wt, n);       // C^T W_u
+        dg(w, st, false, false, nc, b, b, 1.0, w.Wt, n, Tu, b, 0.0, w.Wt2, n);        // (C^T W_u) T_u
+        dg(w, st, false, true, mi, nc, b, -1.0, Wu, ldwu, w.Wt2, n, 1.0, Cm, m);      // C -= W_u (.)^T
+      }
       ++steps;
       k_done = f2;
       if (svd_side && steps - svd_done >= kSvdChunk) {
@@ -535,6 +677,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         // the host during the loop (-7 ms); device calls fold at the end, where
         // the folds hide behind the last SVD chunk
         if (on_final && folded < chunks.size()) {  // a chunk that ended at least one chunk ago
+          ensure_lu();
           fold_chunk(chunks[folded]);
           if (on_final) on_final(b * chunks[folded].s1);
           ++folded;
@@ -543,6 +686,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       }
       if (o.tol > 0.0) {
         double t2 = 0.0;
+        ensure_lu();
         fro2(st, m - e2, n - f2, T + e2 + f2 * m, m, w.nrm, w.scal);
         RUTV_CK(cudaMemcpyAsync(&t2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
         RUTV_CK(cudaStreamSynchronize(st));
@@ -551,6 +695,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       }
     } else {
       // ---- final block: economical SVD of T(r0:m, r0:n)
+      ensure_lu();
       final_block = true;
       r0f = r0; mif = mi; nif = ni;
       if (mi > ni) {
@@ -578,6 +723,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       break;
     }
   }
+  ensure_lu();
   if (!final_block && !stopped) k_done = std::min(k_done, std::min(m, n));
   const int64_t kf = std::min(mif, nif);  // order of the final block's SVD
   if (nflags > 0) {  // optimistic CholeskyQR decisions: one read for the whole loop

@@ -142,6 +142,17 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
 // H_1 ... H_b = I - V Tw V^T.  LAPACK dlarfg sign convention (R3).
 int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr, double* tau,
              double* Tw, int64_t ldt, const QrWork& w);
+// panel_qr's CholeskyQR2 path in two parts, for callers that overlap the
+// reconstruction with work needing only Q1 = V R1^-1 (optimistic mode only:
+// begin returns false -- nothing enqueued -- when that path is unavailable).
+// begin: G1 = V^T V, R1, Q1 -> w.q1 (m x b, ld m).  finish: second pass +
+// reconstruction, exactly panel_qr's outputs (V = W, R, tau, Tw), the decision
+// flag in the next dev_flags slot; afterwards W(b:m, :) = -Q1(b:m, :) M with
+// M = panel_qr_M(w, b, &ldm) (valid until the next panel QR on this workspace).
+bool panel_qr_begin(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const QrWork& w);
+void panel_qr_finish(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr,
+                     double* tau, double* Tw, int64_t ldt, const QrWork& w);
+const double* panel_qr_M(const QrWork& w, int64_t b, int64_t* ldm);
 // Q1 = (I - V Tw V^T)[:, :b] (thin explicit Q), written to Q (m x b).
 void thin_q(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const double* Tw, int64_t ldt,
             double* Q, int64_t ldq, double* tmp_bb, double* part, size_t part_elems);

@@ -612,6 +612,40 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
   return panel_qr_hh(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
 }
 
+bool panel_qr_begin(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const QrWork& w) {
+  if (b <= 0 || m < b || !cholqr_ok(w, m, b)) return false;
+  if (!(w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap)) return false;  // optimistic mode only
+  GemmRole role(C_GEMM_QR);
+  SmallWork sw = carve_small(w.small, b);
+  const int bp = sw.bp;
+  dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);  // G1 (upper)
+  small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
+  dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems, 0, true);  // Q1
+  return true;
+}
+
+void panel_qr_finish(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, double* R, int64_t ldr,
+                     double* tau, double* Tw, int64_t ldt, const QrWork& w) {
+  GemmRole role(C_GEMM_QR);
+  SmallWork sw = carve_small(w.small, b);
+  const int bp = sw.bp;
+  dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems, 0, false, true);  // G2
+  sw.flag = w.dev_flags + (*w.flag_count)++;
+  cudaStream_t rs = recon_side_stream();
+  cudaEvent_t ef = recon_event(0), ej = recon_event(1);
+  small_recon(st, b, sw, w.q1, m, R, ldr, tau, Tw, ldt, w.part, w.part_elems, rs, ef, ej, w.orth_tol);
+  if (m > b)  // W(b:m, :) = -Q1(b:m, :) R2^-1 U~^-1
+    dgemm(st, false, false, m - b, b, b, -1.0, w.q1 + b, m, sw.M, bp, 0.0, V + b, ldv, w.part, w.part_elems, 0, true);
+  small_put_unit_lower(st, b, sw, V, ldv);
+  RUTV_CK(cudaStreamWaitEvent(st, ej, 0));  // T_w, tau, R_h
+}
+
+const double* panel_qr_M(const QrWork& w, int64_t b, int64_t* ldm) {
+  SmallWork sw = carve_small(w.small, b);
+  *ldm = sw.bp;
+  return sw.M;
+}
+
 int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, double* Q, int64_t ldq, double* tmp_bb,
             double* Tmp_bb, double* tau, const QrWork& w) {
   if (cholqr_ok(w, m, b)) {

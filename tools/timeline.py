@@ -51,3 +51,8 @@ for s, ev in sorted(by_stream.items()):
           f"idle gaps {sum(gaps):.2f} ms in {len(gaps)} gaps (>20us: {sum(g for g in gaps if g > 0.02):.2f} ms)")
     for cls, v in busy.most_common():
         print(f"    {cls:18s} {v:8.2f} ms")
+out = os.environ.get("TIMELINE_OUT")
+if out:  # raw per-launch records for offline analysis
+    import json
+    with open(out, "w") as f:
+        json.dump(tl, f)
