@@ -27,6 +27,8 @@ struct GemmRole {
 };
 void count_launch(int cls, int n = 1);
 long long launches_total();
+void launches_by_class(long long* out);  // K_NCLASS counters
+bool prof_active();                      // per-launch event timing on (randutv_profile_begin)
 struct ProfScope {
   ProfScope(cudaStream_t st, int cls, double flops);
   ~ProfScope();

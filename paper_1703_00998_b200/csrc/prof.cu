@@ -50,6 +50,12 @@ static inline int resolve(int cls) { return cls == K_GEMM ? g_role : cls; }
 
 void count_launch(int cls, int n) { g_launches[resolve(cls)].fetch_add(n, std::memory_order_relaxed); }
 
+void launches_by_class(long long* out) {
+  for (int i = 0; i < K_NCLASS; ++i) out[i] = g_launches[i].load();
+}
+
+bool prof_active() { return g_on; }
+
 long long launches_total() {
   long long s = 0;
   for (int i = 0; i < K_NCLASS; ++i) s += g_launches[i].load();

@@ -182,3 +182,36 @@ def test_tall_factorization_with_uv_beyond_leaf():
     ref = oracle.randutv(A, b, q, seed, build_ortho=False)
     par = check_parity(Th, ref["T"], ref["a_fro"])
     assert par["diag_ok"] and par["ek_ok"], par
+
+
+@pytest.mark.parametrize("uv,name,scale", [(False, "c2", 0.2), (True, "c1", 1.0), (False, "c4", 0.05)])
+def test_graph_replay_bitwise(uv, name, scale):
+    """A call repeated with the same arguments is captured into a CUDA graph on
+    its second occurrence and replayed afterwards: every occurrence gives the
+    same bits, and each counts the same number of kernel launches."""
+    c = testmat.config(name, scale=scale)
+    A = to_dev(c.A)
+    m, n = c.A.shape
+    T = P.empty_cm(m, n)
+    U = P.empty_cm(m, m) if uv else None
+    V = P.empty_cm(n, n) if uv else None
+    outs, counts = [], []
+    for _ in range(4):                                     # eager, capture, replay, replay
+        l0 = P.launch_count()
+        _, T, _, info = P.randutv(A, c.b, c.q, c.seed, with_uv=uv, out=(U, T, V))
+        torch.cuda.synchronize()
+        counts.append(P.launch_count() - l0)
+        outs.append((T.clone(), U.clone() if uv else None, V.clone() if uv else None, info))
+    for T_, U_, V_, info_ in outs[1:]:
+        assert torch.equal(T_, outs[0][0])
+        if uv:
+            assert torch.equal(U_, outs[0][1]) and torch.equal(V_, outs[0][2])
+        assert info_.k_done == outs[0][3].k_done and info_.steps == outs[0][3].steps
+    assert len(set(counts)) == 1, counts
+    # a different seed is a different graph: the result must change and match its own eager run
+    _, T2, _, _ = P.randutv(A, c.b, c.q, c.seed + 1, with_uv=False)
+    torch.cuda.synchronize()
+    assert not torch.equal(T2, outs[0][0])
+    ref = oracle.randutv(c.A, min(c.b, m, n), c.q, c.seed, build_ortho=False)
+    par = check_parity(to_host(outs[-1][0]), ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
