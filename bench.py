@@ -72,7 +72,9 @@ def workload_desc(case, m, n):
         if case.name != "c5" else f"c5: {m}x{n}, b={case.b}, q={case.q}, k_stop={case.k_stop}",
         "m": m, "n": n, "b": case.b, "q": case.q, "reortho": True, "mode": "T",
         "flops_formula": "(5+2q)mn^2-(3+2q)n^3/3 (PAPER.md:1205)",
-        "l2": "inputs larger than L2 (A = %.0f MB > 126 MB), re-read every step" % (m * n * 8 / 1e6),
+        "l2": ("inputs larger than L2 (A = %.0f MB > 126 MB), re-read every step" % (m * n * 8 / 1e6))
+        if m * n * 8 > 126e6 else ("A = %.1f MB fits in L2 (not flushed; a parity-size config, not the "
+                                   "driver's bench line)" % (m * n * 8 / 1e6)),
     }
 
 
@@ -160,6 +162,47 @@ def oracle_sample(A_host, case, reps=1):
     return f / t / 1e9, t, f, cores
 
 
+def critical_path(tl):
+    """Breakdown of the critical (first-used) stream of one profiled
+    factorization (per-launch (class, stream slot, start, end) from the
+    library's event timeline): busy time by class, idle time (waits on side
+    streams and launch gaps), and the latency-bound QR-chain time that no GEMM
+    on another stream overlaps (exposed)."""
+    if not tl:
+        return None
+    main = sorted((a, e, c) for c, s, a, e in tl if s == 0)
+    span = max(e for _, _, _, e in tl) - min(a for _, _, a, _ in tl)
+    busy = {}
+    for a, e, c in main:
+        busy[c] = busy.get(c, 0.0) + (e - a)
+    others = sorted((a, e) for c, s, a, e in tl if s != 0 and c.startswith("gemm_"))
+
+    def covered(a, e):  # length of [a, e] covered by other-stream GEMMs
+        tot, cur_a, cur_e = 0.0, None, None
+        for x, y in others:
+            if y <= a or x >= e:
+                continue
+            x, y = max(x, a), min(y, e)
+            if cur_e is None or x > cur_e:
+                if cur_e is not None:
+                    tot += cur_e - cur_a
+                cur_a, cur_e = x, y
+            else:
+                cur_e = max(cur_e, y)
+        if cur_e is not None:
+            tot += cur_e - cur_a
+        return tot
+    chain = [(a, e) for a, e, c in main if c in ("qr_small", "gemm_panel_qr")]
+    chain_ms = sum(e - a for a, e in chain)
+    exposed = sum((e - a) - covered(a, e) for a, e in chain)
+    return {"factorization_span": round(span, 3), "main_busy": round(sum(busy.values()), 3),
+            "main_idle": round(span - sum(busy.values()), 3),
+            "main_by_class": {k: round(v, 3) for k, v in sorted(busy.items(), key=lambda t: -t[1])},
+            "qr_chain_main": round(chain_ms, 3), "qr_chain_main_exposed": round(exposed, 3),
+            "note": "one profiled (eager, per-launch event-timed) factorization; idle = waits for side-stream "
+                    "work (trailing update, panel QR, look-ahead left update, last SVD chunk) and launch gaps"}
+
+
 def make_input(case_name, device, rank, scale=1.0):
     import testmat
     At, case = testmat.device_config(case_name, device=device, scale=scale)
@@ -187,8 +230,12 @@ def run_reference(args):
         c = testmat.config(case_name, scale=scale)
         A_host, case = c.A, c
     m, n = A_host.shape
-    for _ in range(max(args.warmup, 0)):
-        pass  # the oracle has no warm-up state; warm-up steps are skipped to bound the run time
+    # warm-up samples (thread pools, page faults), capped at ~20 s of CPU time
+    warm, t_warm = 0, 0.0
+    while warm < args.warmup and t_warm < 20.0:
+        _, t, _, _ = oracle_sample(A_host, case)
+        warm += 1
+        t_warm += t
     vals, ts = [], []
     for _ in range(args.steps):
         v, t, f, cores = oracle_sample(A_host, case)
@@ -196,11 +243,15 @@ def run_reference(args):
         ts.append(t)
     value = statistics.median(vals)
     sample = f"first randomized step of {case_name} (k_stop=b={case.b}, q={case.q}, T-only) on the full {m}x{n} input"
+    cfg = workload_desc(case, m, n)
+    cfg["workload"] = (f"{case_name}: {m}x{n} fp64, b={case.b}, q={case.q}, T-only -- FIRST RANDOMIZED STEP ONLY "
+                       f"(k_stop = b = {case.b}; a bounded sample of the full factorization, rate in the same unit)")
+    cfg["sample_flops"] = f
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(ts), 3),
+        "steps": args.steps, "warmup": warm, "ms_per_step": round(1e3 * statistics.median(ts), 3),
         "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_desc(case, m, n),
+        "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -282,36 +333,55 @@ def main():
         ms, launches = float(t[0].item()), int(tl[1].item())
     value = F / (ms * 1e-3) / 1e9  # whole-job flops (the factorization's flop count) / time
 
-    # ---------------------------------------------------------------- roofline of the dominant kernel class
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    # One profiled factorization (per-launch CUDA events on each launch's own
+    # stream, inside the library; graph replay is off while profiling).  The
+    # dominant kernel is the sketch DGEMM class (Y = X^T G, Z = X Y, Y = X^T Z:
+    # ~51 % of the flops and the largest share of device time); its launches
+    # run on the critical stream, mostly alone.  The other GEMM roles run
+    # concurrently on side streams, so their per-launch event durations include
+    # sharing the SMs -- listed in by_class, not used as the headline.
     P.profile_begin()
     step()
     prof = P.profile_end()
+    tl = P.profile_timeline()
     gemm = {k: v for k, v in prof.items() if k.startswith("gemm_")}
     g_ms = sum(v["ms"] for v in gemm.values())
-    g_fl = sum(v["flops"] for v in gemm.values())
     g_n = sum(v["launches"] for v in gemm.values())
     tot_ms = sum(v["ms"] for v in prof.values())
-    achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-    traffic = None
+    sk = prof["gemm_sketch"]
+    achieved = sk["flops"] / (sk["ms"] * 1e-3) / 1e12 if sk["ms"] > 0 else 0.0
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_launch")
+            tj = json.load(open(tf))
+            traffic = tj.get("bytes_per_launch")
+            traffic_src = "stored_ncu: " + tj.get("source", "profiles/gemm_traffic.json") + " (not measured in this run)"
         except Exception:  # noqa: BLE001
             traffic = None
+    # the method's algorithmic bytes of one sketch launch Y = X^T G at step 1: X and G read, Y written
+    alg_bytes = 8 * (m * n + m * case.b + n * case.b)
     roofline = {
         "bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": traffic,
-        "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, all GEMM roles incl. split-K reduce)",
+        "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_source": traffic_src,
+        "algorithmic_bytes_step1_launch": alg_bytes,
+        "kernel": "dgemm_kernel, sketch role (X^T G, X Y, X^T Z; FP64 DMMA m8n8k4, incl. its split-K reduce)",
+        "flops_per_launch": "2 m_i n_i b (sum over the class: (2+4q) sum_i m_i n_i b, SURVEY 8(d))",
         "peak_source": "measured DMMA peak, tools/fp64_peaks.cu (profiles/r01_fp64_peaks.md); "
                        "MEASURED_PEAKS.json has no fp64 entry",
-        "gemm_launches": g_n, "gemm_share_of_event_time": round(g_ms / tot_ms, 4) if tot_ms else None,
+        "sketch_launches": sk["launches"], "sketch_ms": round(sk["ms"], 3),
+        "all_gemm": {"launches": g_n, "event_ms": round(g_ms, 3),
+                     "tflops_per_event_time": round(sum(v["flops"] for v in gemm.values()) / (g_ms * 1e-3) / 1e12, 3)
+                     if g_ms > 0 else None,
+                     "share_of_event_time": round(g_ms / tot_ms, 4) if tot_ms else None},
         "by_class": {k: {"ms": round(v["ms"], 3), "tflops": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2)
                          if v["ms"] > 0 and v["flops"] > 0 else None, "launches": v["launches"]}
                      for k, v in prof.items()},
     }
     if use_dist:
         roofline["note"] = "rank 0's kernels; per-class event times include waits on collectives"
+    critical = critical_path(tl)
 
     # ---------------------------------------------------------------- U,V formed (context, single GPU)
     utv = None
@@ -401,7 +471,8 @@ def main():
             "pct_fp64_peak": round(100 * value / world / 1e3 / FP64_DMMA_PEAK_TFLOPS, 2),
             "pct_cublas_dgemm": round(100 * value / world / 1e3 / FP64_CUBLAS_DGEMM_TFLOPS, 2),
             "time_to_factor_s": round(ms * 1e-3, 4),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "roofline": roofline, "critical_path_ms": critical, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches,
             "utv": utv,
             "paper_context": PAPER_CONTEXT if case.name == "c3" else None,
         }
