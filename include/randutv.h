@@ -208,7 +208,13 @@ typedef struct randutv_comm randutv_comm;
  * libnccl.so.2, e.g. torch's); RANDUTV_ERR_NCCL if unavailable. */
 RANDUTV_API int randutv_nccl_unique_id(void* id_out);
 /* NCCL communicator for ``rank`` of ``nranks`` on the current CUDA device
- * (collective: every rank must call it).  Released by randutv_comm_destroy. */
+ * (collective: every rank must call it).  Released by randutv_comm_destroy.
+ * Failure handling: every host wait of randutv_factor_dist polls
+ * ncclCommGetAsyncError; an asynchronous error, or a wait longer than
+ * RANDUTV_NCCL_TIMEOUT_S seconds (read at creation, default 600) -- e.g. a peer
+ * that died -- aborts the communicator (ncclCommAbort) and the call returns
+ * RANDUTV_ERR_NCCL; later calls on an aborted communicator return
+ * RANDUTV_ERR_NCCL at once (destroy it and create a new one). */
 RANDUTV_API int randutv_comm_init_nccl(int32_t nranks, int32_t rank, const void* id, randutv_comm** out);
 /* Loopback communicator: this process drives all ``nranks`` ranks on the
  * current device, each with its own shard; collectives are device copies/sums
@@ -216,6 +222,12 @@ RANDUTV_API int randutv_comm_init_nccl(int32_t nranks, int32_t rank, const void*
  * another rank).  It checks the distributed arithmetic on one GPU. */
 RANDUTV_API int randutv_comm_init_loopback(int32_t nranks, randutv_comm** out);
 RANDUTV_API int randutv_comm_destroy(randutv_comm* comm);
+/* Collectives issued on ``comm`` since its creation (one per call of the
+ * factorization, whatever the number of local ranks) and their payload per
+ * rank in bytes: [0] allreduce, [1] broadcast, [2] allgather (either pointer
+ * may be NULL).  Returns 0, or RANDUTV_ERR_NCCL if the communicator was
+ * aborted. */
+RANDUTV_API int randutv_comm_stats(const randutv_comm* comm, long long* counts, long long* bytes);
 /* Ranks driven by this process: returns their count (1 for NCCL, nranks for
  * loopback), writes the world size and up to max_ranks rank ids. */
 RANDUTV_API int randutv_comm_local_ranks(const randutv_comm* comm, int32_t* world, int32_t* ranks_out,

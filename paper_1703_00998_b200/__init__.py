@@ -109,7 +109,7 @@ EXPORTED = ["randutv_factor", "randutv_factor_ex", "randutv_workspace_size", "ra
             "randutv_profile_end", "randutv_profile_class_name", "randutv_profile_timeline", "randutv_nccl_unique_id",
             "randutv_comm_init_nccl", "randutv_comm_init_loopback", "randutv_comm_destroy",
             "randutv_comm_local_ranks", "randutv_dist_local_cols", "randutv_dist_global_col",
-            "randutv_factor_dist", "randutv_rsvd"]
+            "randutv_factor_dist", "randutv_rsvd", "randutv_comm_stats"]
 
 
 def launch_count() -> int:

@@ -28,10 +28,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/randutv.h"
@@ -62,6 +65,18 @@ struct Comm {
   int P = 1;                // world size
   std::vector<int> ranks;   // global ranks this process drives (1 for NCCL, P for loopback)
   int dev = 0;
+  bool aborted = false;     // NCCL: aborted after an asynchronous error or a timeout; unusable
+  // collectives issued (one per call, whatever the number of local ranks) and
+  // their payload per rank in bytes: [0] allreduce, [1] broadcast, [2] allgather
+  long long ncoll[3] = {0, 0, 0}, nbytes[3] = {0, 0, 0};
+  void note(int kind, size_t count) {
+    ++ncoll[kind];
+    nbytes[kind] += (long long)(count * sizeof(double));
+  }
+  // host waits (the only ones of the distributed factorization): NCCL
+  // overrides them to poll for asynchronous communicator errors and a timeout
+  virtual void sync(cudaStream_t st) { RUTV_CK(cudaStreamSynchronize(st)); }
+  virtual void sync_event(cudaEvent_t e) { RUTV_CK(cudaEventSynchronize(e)); }
   // in-place sum over all ranks of bufs[l] (count doubles each)
   virtual void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) = 0;
   // bufs[l] <- bufs[root]
@@ -90,18 +105,21 @@ struct LoopComm : Comm {
     RUTV_CK(cudaGetDevice(&dev));
   }
   void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) override {
+    note(0, count);
     // fixed order: ((b0 + b1) + b2) + ...  accumulated in b0, then copied out
     for (int r = 1; r < P; ++r) add_into(st, count, bufs[r], bufs[0]);
     for (int r = 1; r < P; ++r)
       if (count) RUTV_CK(cudaMemcpyAsync(bufs[r], bufs[0], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   void bcast(const std::vector<double*>& bufs, size_t count, int root, cudaStream_t st) override {
+    note(1, count);
     for (int r = 0; r < P; ++r)
       if (r != root && count)
         RUTV_CK(cudaMemcpyAsync(bufs[r], bufs[root], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   void allgather(const std::vector<double*>& send, const std::vector<double*>& recv, size_t count,
                  cudaStream_t st) override {
+    note(2, count);
     for (int l = 0; l < P; ++l)
       for (int r = 0; r < P; ++r)
         if (count)
@@ -120,6 +138,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;  // optional
+  ncclResult_t (*Abort)(ncclComm_t) = nullptr;                         // optional
 };
 
 NcclApi& nccl() {
@@ -136,6 +156,8 @@ NcclApi& nccl() {
     api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
     api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
     api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.GetAsyncError = (decltype(api.GetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.Abort = (decltype(api.Abort))dlsym(h, "ncclCommAbort");
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
              api.AllGather;
   });
@@ -153,24 +175,69 @@ struct NcclError {
 
 struct NcclComm : Comm {
   ncclComm_t c = nullptr;
+  double timeout_s = 600.0;  // RANDUTV_NCCL_TIMEOUT_S at creation: a host wait longer than this aborts
   NcclComm(int p, int rank, const ncclUniqueId& id) {
     P = p;
     ranks.push_back(rank);
     RUTV_CK(cudaGetDevice(&dev));
+    if (const char* e = getenv("RANDUTV_NCCL_TIMEOUT_S")) timeout_s = atof(e);
     RUTV_NCCL(nccl().CommInitRank(&c, p, id, rank));
   }
   ~NcclComm() override {
     if (c) nccl().CommDestroy(c);
   }
+  ncclComm_t live() {
+    if (aborted || !c) throw NcclError{ncclInvalidUsage};
+    return c;
+  }
+  void abort_comm() {
+    aborted = true;
+    if (c && nccl().Abort) nccl().Abort(c);  // unblocks kernels waiting on dead peers
+    c = nullptr;
+  }
+  // Wait until query() reports completion, polling ncclCommGetAsyncError (a
+  // failed peer or network error) and the timeout (a peer that never arrives);
+  // either aborts the communicator and throws -> RANDUTV_ERR_NCCL.
+  template <class Q>
+  void wait_for(Q query) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 0;; ++it) {
+      const cudaError_t e = query();
+      if (e == cudaSuccess) return;
+      if (e != cudaErrorNotReady) RUTV_CK(e);
+      ncclResult_t ae = ncclSuccess;
+      if (c && nccl().GetAsyncError && nccl().GetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess &&
+          ae != ncclInProgress) {
+        abort_comm();
+        throw NcclError{ae};
+      }
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > timeout_s) {
+        fprintf(stderr, "randutv: NCCL collective not complete after %.3g s: aborting the communicator\n", el);
+        abort_comm();
+        throw NcclError{ncclSystemError};
+      }
+      if (it > 2000) std::this_thread::sleep_for(std::chrono::microseconds(20));  // spin first, then back off
+    }
+  }
+  void sync(cudaStream_t st) override {
+    wait_for([&] { return cudaStreamQuery(st); });
+  }
+  void sync_event(cudaEvent_t ev) override {
+    wait_for([&] { return cudaEventQuery(ev); });
+  }
   void allreduce(const std::vector<double*>& bufs, size_t count, cudaStream_t st) override {
-    if (count) RUTV_NCCL(nccl().AllReduce(bufs[0], bufs[0], count, ncclFloat64, ncclSum, c, st));
+    note(0, count);
+    if (count) RUTV_NCCL(nccl().AllReduce(bufs[0], bufs[0], count, ncclFloat64, ncclSum, live(), st));
   }
   void bcast(const std::vector<double*>& bufs, size_t count, int root, cudaStream_t st) override {
-    if (count) RUTV_NCCL(nccl().Broadcast(bufs[0], bufs[0], count, ncclFloat64, root, c, st));
+    note(1, count);
+    if (count) RUTV_NCCL(nccl().Broadcast(bufs[0], bufs[0], count, ncclFloat64, root, live(), st));
   }
   void allgather(const std::vector<double*>& send, const std::vector<double*>& recv, size_t count,
                  cudaStream_t st) override {
-    if (count) RUTV_NCCL(nccl().AllGather(send[0], recv[0], count, ncclFloat64, c, st));
+    note(2, count);
+    if (count) RUTV_NCCL(nccl().AllGather(send[0], recv[0], count, ncclFloat64, live(), st));
   }
 };
 
@@ -375,10 +442,10 @@ void dg(const RankWork& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t
   dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, w.part, w.part_elems, 0, b_upper);
 }
 
-int read_int_sync(cudaStream_t st, const int* d) {
+int read_int_sync(Comm& comm, cudaStream_t st, const int* d) {
   int h = 0;
   RUTV_CK(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
-  RUTV_CK(cudaStreamSynchronize(st));
+  comm.sync(st);
   return h;
 }
 
@@ -606,7 +673,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
     // pack [sum of squares, non-finite flag, T aliases A] and allreduce
     for (auto& lr : L) {
       RUTV_CK(cudaMemcpyAsync(lr.w.pack, lr.w.scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
-      int hf = read_int_sync(st, lr.w.flag);
+      int hf = read_int_sync(comm, st, lr.w.flag);
       double fv[2] = {hf ? 1.0 : 0.0, 0.0};
       if (lr.nl > 0) {  // an in-place factorization cannot be redone from A
         const char* a0 = (const char*)lr.A;
@@ -616,12 +683,12 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         fv[1] = (t0 < a1 && a0 < t1) ? 1.0 : 0.0;
       }
       RUTV_CK(cudaMemcpyAsync(lr.w.pack + 1, fv, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
-      RUTV_CK(cudaStreamSynchronize(st));
+      comm.sync(st);
     }
     comm.allreduce(bufs(&RankWork::pack), 3, st);
     double h[3];
     RUTV_CK(cudaMemcpyAsync(h, L[0].w.pack, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    RUTV_CK(cudaStreamSynchronize(st));
+    comm.sync(st);
     if (h[1] != 0.0) return RANDUTV_ERR_NONFINITE;
     a_fro_ = std::sqrt(h[0]);
     if (h[2] != 0.0) opt_ = false;
@@ -769,7 +836,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
             } else {
               double h[3];
               RUTV_CK(cudaMemcpyAsync(h, small_of(L[0], bw).stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-              RUTV_CK(cudaStreamSynchronize(st));
+              comm.sync(st);
               ok = o.qr_mode == 0 && h[0] == 0.0 && h[2] <= 1e4 * h[1];
             }
             if (ok) {
@@ -815,22 +882,28 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
             dg(lr.w, st, false, false, nt[l], b, b, 1.0, lr.w.Y, std::max<int64_t>(nt[l], 1), lr.sw.R1i, bp, 0.0,
                lr.w.q1, std::max<int64_t>(nt[l], 1), true);
           }
-          dist_gram_chol(&RankWork::q1, nt, 2, b);
-          // top b x b block of Q1 (global rows 0..b-1 = first local block of the owner) -> every rank
+          // G2 = Q1^T Q1 (partial Grams) and the top b x b block of Q1 (global rows
+          // 0..b-1 = the owner's first local block; the other ranks contribute
+          // exact zeros, so the sum is that block bit for bit) in ONE allreduce
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
-            if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, std::max<int64_t>(nt[l], 1), lr.w.pack, b);
+            const int64_t ldq = std::max<int64_t>(nt[l], 1);
+            dg(lr.w, st, true, false, b, b, nt[l], 1.0, lr.w.q1, ldq, lr.w.q1, ldq, 0.0, lr.w.pack, b);
+            if (lr.r == owner) copy_matrix(st, b, b, lr.w.q1, ldq, lr.w.pack + size_t(b) * b, b);
+            else set_zero(st, b, b, lr.w.pack + size_t(b) * b, b);
           }
-          comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
+          comm.allreduce(bufs(&RankWork::pack), 2 * size_t(b) * b, st);
           for (size_t l = 0; l < L.size(); ++l) {
             auto& lr = L[l];
+            copy_matrix(st, b, b, lr.w.pack, b, lr.sw.W2, lr.sw.bp);
             SmallWork sw = lr.sw;
             if (opt_y && ny < kDistYFlags) sw.flag = lr.w.qflags + lr.w.qflags_cap + ny;
-            small_recon(st, b, sw, lr.w.pack, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b, lr.w.part, lr.w.part_elems);
+            small_recon(st, b, sw, lr.w.pack + size_t(b) * b, b, lr.w.Rtmp, b, lr.w.tau, lr.w.Tfin, b, lr.w.part,
+                        lr.w.part_elems);
           }
           const bool qr_flagged = opt_y && ny < kDistYFlags;
           if (qr_flagged) ++ny;
-          qr_ok = qr_flagged ? true : (read_int_sync(st, L[0].sw.flag) == 0);
+          qr_ok = qr_flagged ? true : (read_int_sync(comm, st, L[0].sw.flag) == 0);
           if (qr_ok) {
             for (size_t l = 0; l < L.size(); ++l) {
               auto& lr = L[l];
@@ -872,7 +945,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       int ny = sketch_qr_p(opt_);
       if (ny < 0) return lam_err;
       if (ny > 0) {
-        RUTV_CK(cudaEventSynchronize(ev_yflags_));
+        comm.sync_event(ev_yflags_);
         bool failed = false;
         for (int f = 0; f < ny; ++f) failed |= h_yflags_[f] != 0;
         if (failed && sketch_qr_p(false) < 0) return lam_err;
@@ -967,7 +1040,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         comm.allreduce(bufs(&RankWork::pack), 1, st);
         double t2 = 0.0;
         RUTV_CK(cudaMemcpyAsync(&t2, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
-        RUTV_CK(cudaStreamSynchronize(st));
+        comm.sync(st);
         if (std::sqrt(t2) <= o.tol * a_fro_) break;
       }
     } else {
@@ -1036,16 +1109,16 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       if (nflags_[l] > 0) {
         std::vector<int> hf(nflags_[l]);
         RUTV_CK(cudaMemcpyAsync(hf.data(), L[l].w.qflags, sizeof(int) * hf.size(), cudaMemcpyDeviceToHost, st));
-        RUTV_CK(cudaStreamSynchronize(st));
+        comm.sync(st);
         for (int f : hf) any += f ? 1.0 : 0.0;
       }
       RUTV_CK(cudaMemcpyAsync(L[l].w.pack, &any, sizeof(double), cudaMemcpyHostToDevice, st));
-      RUTV_CK(cudaStreamSynchronize(st));
+      comm.sync(st);
     }
     comm.allreduce(bufs(&RankWork::pack), 1, st);
     double tot = 0.0;
     RUTV_CK(cudaMemcpyAsync(&tot, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
-    RUTV_CK(cudaStreamSynchronize(st));
+    comm.sync(st);
     if (tot != 0.0) {
       drop_events();
       return kDistRetry;
@@ -1069,17 +1142,24 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
   }
   for (const SvdChunk& ch : chunks) {
   if (ch.done) RUTV_CK(cudaStreamWaitEvent(st, ch.done, 0));
+  // the chunk's Us (each computed by its step's owner) -> every rank, for the
+  // row folds: ONE allreduce of the chunk's slots, every slot but the owner's
+  // zero on each rank (the sum is the owner's block bit for bit)
+  const int64_t cnt = ch.s1 - ch.s0;
+  for (auto& lr : L) {
+    set_zero(st, b, cnt * b, lr.w.pack, b);
+    for (int64_t si = ch.s0; si < ch.s1; ++si)
+      if (lr.r == int(si % P))
+        copy_matrix(st, b, b, lr.w.Usall + size_t(si / P) * b * b, b, lr.w.pack + size_t(si - ch.s0) * b * b, b);
+  }
+  comm.allreduce(bufs(&RankWork::pack), size_t(cnt) * b * b, st);
   for (int64_t si = ch.s0; si < ch.s1; ++si) {
     const int64_t r0 = b * si;
     const int owner = int(si % P);
     const int64_t js = si / P;  // the owner's slot of step si
-    // Us of step si (computed by its owner) -> every rank, for the row fold
-    for (auto& lr : L)
-      if (lr.r == owner) copy_matrix(st, b, b, lr.w.Usall + size_t(js) * b * b, b, lr.w.pack, b);
-    comm.bcast(bufs(&RankWork::pack), size_t(b) * b, owner, st);
     for (size_t l = 0; l < L.size(); ++l) {
       auto& lr = L[l];
-      const double* Us = lr.w.pack;
+      const double* Us = lr.w.pack + size_t(si - ch.s0) * b * b;
       const double* Vs = lr.w.Vsall + size_t(js) * b * b;  // used on the owner only
       const int64_t cb = b * blocks_before(si, lr.r, P);  // local offset of block si (if owned) / of J3
       const int64_t cs = cb + ((lr.r == owner) ? b : 0), nc = lr.nl - cs;
@@ -1175,7 +1255,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
       RUTV_CK(cudaMemcpyAsync(&t2, L[0].w.pack, sizeof(double), cudaMemcpyDeviceToHost, st));
       info->trailing_fro = std::sqrt(t2);
     }
-    RUTV_CK(cudaStreamSynchronize(st));
+    comm.sync(st);
   }
   return RANDUTV_OK;
 }
@@ -1261,25 +1341,26 @@ void DistFactor::form_uv(int64_t steps, bool final_block, bool final_fat, int64_
 }
 
 std::mutex g_dmu;
-void* g_dws = nullptr;
-size_t g_dws_bytes = 0;
+void* g_dws[kMaxDevices] = {};        // cached workspace, per device
+size_t g_dws_bytes[kMaxDevices] = {};
 
 void* dist_ws(size_t bytes) {
-  if (bytes > g_dws_bytes) {
-    if (g_dws) {
-      cudaDeviceSynchronize();
-      cudaFree(g_dws);
-      g_dws = nullptr;
-      g_dws_bytes = 0;
+  const int d = current_device();
+  if (bytes > g_dws_bytes[d]) {
+    if (g_dws[d]) {
+      RUTV_CK(cudaDeviceSynchronize());
+      cudaFree(g_dws[d]);
+      g_dws[d] = nullptr;
+      g_dws_bytes[d] = 0;
     }
-    if (cudaMalloc(&g_dws, bytes) != cudaSuccess) {
+    if (cudaMalloc(&g_dws[d], bytes) != cudaSuccess) {
       cudaGetLastError();
-      g_dws = nullptr;
+      g_dws[d] = nullptr;
       return nullptr;
     }
-    g_dws_bytes = bytes;
+    g_dws_bytes[d] = bytes;
   }
-  return g_dws;
+  return g_dws[d];
 }
 
 }  // namespace
@@ -1341,6 +1422,15 @@ int randutv_comm_destroy(randutv_comm* c) {
   return 0;
 }
 
+int randutv_comm_stats(const randutv_comm* c, long long* counts, long long* bytes) {
+  if (!c) return -1;
+  for (int k = 0; k < 3; ++k) {
+    if (counts) counts[k] = c->c->ncoll[k];
+    if (bytes) bytes[k] = c->c->nbytes[k];
+  }
+  return c->c->aborted ? RANDUTV_ERR_NCCL : 0;
+}
+
 int randutv_comm_local_ranks(const randutv_comm* c, int32_t* world, int32_t* ranks_out, int32_t max_ranks) {
   if (!c) return -1;
   if (world) *world = c->c->P;
@@ -1382,6 +1472,7 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   if (b + o.oversample > RANDUTV_MAX_B) return -1;
   if (b > n) b = n;
   rutv::Comm& c = *comm->c;
+  if (c.aborted) return RANDUTV_ERR_NCCL;  // aborted after an error or a timeout: unusable
   const int nlr = (int)c.ranks.size();
   for (int l = 0; l < nlr; ++l) {
     const int64_t nl = local_cols(n, b, c.ranks[l], c.P);
@@ -1392,6 +1483,11 @@ int randutv_factor_dist(const randutv_opts* opts, randutv_comm* comm, int64_t m,
   }
   std::lock_guard<std::mutex> lock(rutv::g_dmu);
   try {
+    struct Order {  // device-side ordering after the previous library call (CallOrder, driver.cu)
+      cudaStream_t st;
+      explicit Order(cudaStream_t s) : st(s) { rutv::call_order_begin(st); }
+      ~Order() { rutv::call_order_end(st); }
+    } order(o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread);
     rutv::DistPlan d = rutv::make_dist_plan(m, n, b, c.P, uv, o.oversample);
     const size_t per = rutv::dist_rank_bytes(d);
     char* ws = (char*)rutv::dist_ws(per * nlr);

@@ -49,6 +49,24 @@ struct DevState {
 DevState g_dev[kMaxDevices];
 
 DevState& dev_state() { return g_dev[current_device()]; }
+}  // namespace
+
+void rutv::call_order_begin(cudaStream_t st) {
+  DevState& d = dev_state();
+  if (d.last) RUTV_CK(cudaStreamWaitEvent(st, d.last, 0));
+}
+
+void rutv::call_order_end(cudaStream_t st) noexcept {
+  DevState& d = g_dev[std::max(0, std::min(kMaxDevices - 1, [] { int v = 0; cudaGetDevice(&v); return v; }()))];
+  if (!d.last && cudaEventCreateWithFlags(&d.last, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    d.last = nullptr;
+    return;
+  }
+  if (cudaEventRecord(d.last, st) != cudaSuccess) cudaGetLastError();
+}
+
+namespace {
 
 // Scope of one C-ABI call on stream st: st first waits for everything the
 // previous call on this device enqueued (on any stream: all of them are joined
@@ -57,19 +75,8 @@ DevState& dev_state() { return g_dev[current_device()]; }
 // on the same cached workspace at once.
 struct CallOrder {
   cudaStream_t st;
-  explicit CallOrder(cudaStream_t s) : st(s) {
-    DevState& d = dev_state();
-    if (d.last) RUTV_CK(cudaStreamWaitEvent(st, d.last, 0));
-  }
-  ~CallOrder() {
-    DevState& d = dev_state();
-    if (!d.last && cudaEventCreateWithFlags(&d.last, cudaEventDisableTiming) != cudaSuccess) {
-      cudaGetLastError();
-      d.last = nullptr;
-      return;
-    }
-    if (cudaEventRecord(d.last, st) != cudaSuccess) cudaGetLastError();
-  }
+  explicit CallOrder(cudaStream_t s) : st(s) { call_order_begin(st); }
+  ~CallOrder() { call_order_end(st); }
 };
 
 struct Plan {

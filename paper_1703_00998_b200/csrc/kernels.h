@@ -11,6 +11,12 @@ namespace rutv {
 
 int num_sms();
 
+// Device-side ordering of C-ABI calls (driver.cu): every call's stream first
+// waits for the end of the previous call's work on the same device (the cached
+// workspaces and shared side streams are reused), and records that end.
+void call_order_begin(cudaStream_t st);
+void call_order_end(cudaStream_t st) noexcept;
+
 // ---- prof.cu: launch counting and optional per-class event timing ---------
 // Kernel classes of the profiler.  GEMMs are attributed to the role the
 // driver is in (set_gemm_role); K_GEMM means "the current role".

@@ -27,6 +27,7 @@ def _lib():
         L.randutv_comm_init_loopback.argtypes = [c_i32, ctypes.POINTER(c_vp)]
         L.randutv_comm_destroy.argtypes = [c_vp]
         L.randutv_comm_local_ranks.argtypes = [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), c_i32]
+        L.randutv_comm_stats.argtypes = [c_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
         L.randutv_dist_local_cols.argtypes = [c_i64, c_i64, c_i32, c_i32]
         L.randutv_dist_local_cols.restype = c_i64
         L.randutv_dist_global_col.argtypes = [c_i64, c_i64, c_i32, c_i32]
@@ -37,7 +38,7 @@ def _lib():
                                           ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
                                           ctypes.POINTER(c_vp), ctypes.POINTER(c_i64), ctypes.POINTER(_Info)]
         for f in ("randutv_nccl_unique_id", "randutv_comm_init_nccl", "randutv_comm_init_loopback",
-                  "randutv_comm_destroy", "randutv_comm_local_ranks", "randutv_factor_dist"):
+                  "randutv_comm_destroy", "randutv_comm_local_ranks", "randutv_factor_dist", "randutv_comm_stats"):
             getattr(L, f).restype = ctypes.c_int
         L._dist_ready = True
     return L
@@ -100,6 +101,18 @@ class Comm:
             raise RandUTVError(nl, "randutv_comm_local_ranks")
         self.world = int(world.value)
         self.ranks = [int(ranks[i]) for i in range(nl)]
+
+    def stats(self) -> dict:
+        """Collectives issued so far and their payload per rank (bytes):
+        {"allreduce": (count, bytes), "bcast": ..., "allgather": ..., "aborted": bool}."""
+        cnt = (ctypes.c_longlong * 3)()
+        byt = (ctypes.c_longlong * 3)()
+        rc = _lib().randutv_comm_stats(self.h, cnt, byt)
+        if rc < 0:
+            raise RandUTVError(rc, "randutv_comm_stats")
+        out = {k: (int(cnt[i]), int(byt[i])) for i, k in enumerate(("allreduce", "bcast", "allgather"))}
+        out["aborted"] = rc != 0
+        return out
 
     def close(self):
         if self.h:

@@ -19,7 +19,7 @@ def header_functions():
 def test_exports_every_declared_symbol():
     L = P.lib()
     names = header_functions()
-    assert len(names) == 25, names
+    assert len(names) == 26, names
     assert sorted(P.EXPORTED) == names
     for name in names:
         assert hasattr(L, name), name

@@ -341,3 +341,69 @@ def test_dist_fat_parity(m, n, b, q, nranks, uv):
     _, T1, _, _ = P.randutv(to_dev(A), b, q, 3, with_uv=False)
     d1, dd = np.abs(np.diag(T1.cpu().numpy())), np.abs(np.diag(T))
     assert np.all(np.abs(d1 - dd) <= 1e-10 * d1 + n * EPS * ref["a_fro"])
+
+
+@pytest.mark.parametrize("m,n,b,q,nranks", [(1000, 1000, 64, 2, 4), (800, 600, 50, 1, 3), (640, 640, 64, 0, 2),
+                                            (1500, 1200, 128, 2, 8)])
+def test_dist_collectives_per_step(m, n, b, q, nranks):
+    """Collectives of one distributed factorization (T-only, tol = 0, CholeskyQR
+    path) against the per-step model of DESIGN.md §8: per randomized step
+    2q + 3 allreduces (q re-orthonormalisation Grams, q Z = X Y, the QR(Y)
+    Gram, the merged second Gram + top block of Q1, P = T W_v) and one
+    broadcast (the panel's W_u, T_u, R11); one allreduce per SVD chunk of 8
+    steps (its Us blocks for the row folds); two per call (||A||_F with the
+    non-finite / aliasing flags, and the CholeskyQR verdict); no allgather."""
+    A = testmat.gaussian(m, n, m + n)
+    comm = D.loopback(nranks)
+    Ad = to_dev(A)
+    shards = [D.shard(Ad, b, r, nranks) for r in range(nranks)]
+    Ts, info = D.factor(comm, shards, m, n, b, q, 3)
+    torch.cuda.synchronize()
+    st = comm.stats()
+    comm.close()
+    S = info.steps
+    chunks = -(-S // 8)
+    assert info.qr_fallbacks == 0
+    assert st["allreduce"][0] == 2 + S * (2 * q + 3) + chunks, (st, S)
+    assert st["bcast"][0] == S, st
+    assert st["allgather"][0] == 0, st
+    assert not st["aborted"]
+    # payload of the per-step allreduces (bytes per rank), step i = 1..S
+    per_step = sum(8 * (q * b * b + q * (m - b * (i - 1)) * b + b * b + 2 * b * b + m * b) for i in range(1, S + 1))
+    assert st["allreduce"][1] == per_step + 8 * (3 + 1) + 8 * b * b * S, (st, per_step)
+    T = D.assemble(Ts, n, b).cpu().numpy()
+    ref = oracle.randutv(A, b, q, 3, build_ortho=False)
+    par = check_parity(T, ref["T"], ref["a_fro"])
+    assert par["diag_ok"] and par["ek_ok"], par
+
+
+def test_dist_nccl_timeout_aborts():
+    """NCCL failure handling: a host wait longer than RANDUTV_NCCL_TIMEOUT_S
+    (here 0 s: the first wait that is not already complete) aborts the
+    communicator (ncclCommAbort) and the call returns RANDUTV_ERR_NCCL; the
+    aborted communicator then refuses further work with RANDUTV_ERR_NCCL."""
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(30200 + os.getpid() % 500)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    old = os.environ.get("RANDUTV_NCCL_TIMEOUT_S")
+    os.environ["RANDUTV_NCCL_TIMEOUT_S"] = "0"
+    try:
+        comm = D.nccl_from_torch()
+        c = testmat.config("c3", scale=0.2)
+        with pytest.raises(P.RandUTVError) as e:
+            D.factor(comm, [to_dev(c.A)], *c.A.shape, c.b, c.q, c.seed)
+        assert e.value.code == 4                      # RANDUTV_ERR_NCCL
+        assert comm.stats()["aborted"]
+        with pytest.raises(P.RandUTVError) as e2:
+            D.factor(comm, [to_dev(c.A)], *c.A.shape, c.b, c.q, c.seed)
+        assert e2.value.code == 4
+        comm.close()
+    finally:
+        if old is None:
+            del os.environ["RANDUTV_NCCL_TIMEOUT_S"]
+        else:
+            os.environ["RANDUTV_NCCL_TIMEOUT_S"] = old
+        torch.cuda.synchronize()
+        dist.destroy_process_group()
