@@ -623,13 +623,17 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
             RUTV_CK(cudaMemcpyAsync(h_yflags, qwy.dev_flags, sizeof(int) * *qwy.flag_count, cudaMemcpyDeviceToHost, st));
             RUTV_CK(cudaEventRecord(ev_yflags, st));
           }
+          // P2 = P T_v = T(:, J2) (L T_v) - P_big (M T_v): two b x b products
+          // replace one m x b x b pass
           set_gemm_role(C_GEMM_RIGHT);
-          ensure_lu();
-          dg(w, st, false, false, m, b, b, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);           // T(:, J2) L
-          RUTV_CK(cudaStreamWaitEvent(st, j, 0));
           int64_t ldm = 0;
           const double* M = panel_qr_M(qwy, b, &ldm);
-          dg(w, st, false, false, m, b, b, -1.0, w.Pbig, m, M, ldm, 1.0, w.P, m);       // - P_big M
+          dg(w, st, false, false, b, b, b, 1.0, Wv, ldwv, Tv, b, 0.0, w.Ttmp, b);        // L T_v
+          dg(w, st, false, false, b, b, b, 1.0, M, ldm, Tv, b, 0.0, w.H, b);             // M T_v
+          ensure_lu();
+          dg(w, st, false, false, m, b, b, 1.0, TJ, m, w.Ttmp, b, 0.0, w.P2, m);         // T(:, J2) L T_v
+          RUTV_CK(cudaStreamWaitEvent(st, j, 0));
+          dg(w, st, false, false, m, b, b, -1.0, w.Pbig, m, w.H, b, 1.0, w.P2, m);       // - P_big M T_v
         } else {
           check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
           if (copy_flags && *qwy.flag_count > 0) {
@@ -639,8 +643,8 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
           set_gemm_role(C_GEMM_RIGHT);
           ensure_lu();
           dg(w, st, false, false, m, b, ni, 1.0, TJ, m, Wv, ldwv, 0.0, w.P, m);
+          dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
         }
-        dg(w, st, false, false, m, b, b, 1.0, w.P, m, Tv, b, 0.0, w.P2, m);
       };
       if (defer_y) {
         sketch_qr_p(w.qw, false, have_y0);  // decisions into the per-call flags

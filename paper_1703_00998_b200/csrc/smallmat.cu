@@ -633,21 +633,37 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
   const int bp = d.bp, b = d.b;
   init_stats(s);
   cl.sync();  // every CTA's stats are initialised before any remote update
-  // ---- deviation of G2 from I (before padding), padding, zero lower tiles
+  // ---- deviation of G2 from I (before padding), padding, zero lower tiles.
+  // This CTA's columns c = cta, cta + C, ... are walked in batches of 16
+  // elements per thread with every load of a batch issued before its stores
+  // (a load-store-load chain through possibly aliasing pointers serialised ~32
+  // L2 round trips per thread: 30-65 us per launch)
+  const int per_cta = ((bp - cta + C - 1) / C) * bp;
   {
     double dev = 0.0;
-    for (int c = cta; c < bp; c += C)
-      for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
-      if (r < b && c < b) {  // the upper triangle (the Gram GEMM writes only that)
-        const double v = (r <= c) ? a.W2[e] - (r == c ? 1.0 : 0.0) : 0.0;
-        dev = fmax(dev, isfinite(v) ? fabs(v) : 1e300);
-      } else {
-        a.W2[e] = (r == c) ? 1.0 : 0.0;
-        a.F[e] = 0.0;
+    for (int base = 0; base < per_cta; base += 16 * SNT) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+        v[u] = (idx < per_cta && r < b && c < b && r <= c) ? __ldcg(a.W2 + c * bp + r) : 0.0;
       }
-      if (r / TS > c / TS) {
-        a.R2[e] = 0.0;
-        a.R2i[e] = 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+        if (idx >= per_cta) continue;
+        const int e = c * bp + r;
+        if (r < b && c < b) {  // the upper triangle (the Gram GEMM writes only that)
+          const double dv = (r <= c) ? v[u] - (r == c ? 1.0 : 0.0) : 0.0;
+          dev = fmax(dev, isfinite(dv) ? fabs(dv) : 1e300);
+        } else {
+          a.W2[e] = (r == c) ? 1.0 : 0.0;
+          a.F[e] = 0.0;
+        }
+        if (r / TS > c / TS) {
+          a.R2[e] = 0.0;
+          a.R2i[e] = 0.0;
+        }
       }
     }
     for (int o = 16; o; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
@@ -669,12 +685,23 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
   // (R2^T R2 = I + U + U^T + O(E^2) = I + E), so the 8-step Cholesky is skipped.
   const double devmax = __longlong_as_double((long long)*cl.map_shared_rank(&s.devbits, 0));
   if (double(b) * devmax <= 1e-8) {
-    for (int c = cta; c < bp; c += C)
-      for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
-      const double ev = (r < b && c < b) ? a.W2[e] - (r == c ? 1.0 : 0.0) : 0.0;
-      const double u = (r < c) ? ev : (r == c ? 0.5 * ev : 0.0);
-      a.R2[e] = (r == c ? 1.0 : 0.0) + u;
-      a.R2i[e] = (r == c ? 1.0 : 0.0) - u;
+    for (int base = 0; base < per_cta; base += 16 * SNT) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+        v[u] = (idx < per_cta && r < b && c < b && r <= c) ? __ldcg(a.W2 + c * bp + r) - (r == c ? 1.0 : 0.0)
+                                                            : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+        if (idx >= per_cta) continue;
+        const int e = c * bp + r;
+        const double uu = (r < c) ? v[u] : (r == c ? 0.5 * v[u] : 0.0);
+        a.R2[e] = (r == c ? 1.0 : 0.0) + uu;
+        a.R2i[e] = (r == c ? 1.0 : 0.0) - uu;
+      }
     }
   } else {
     chol_inv_dev(cl, d, a.W2, a.R2, a.R2i, s);
@@ -706,9 +733,19 @@ __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
   }
   cluster_barrier(cl);
   lu_sign_inv_dev(cl, d, a.F, a.Li, a.Ui, a.S, s);
-  for (int c = cta; c < bp; c += C)  // column-strided: no 64-bit division per element
-    for (int r = threadIdx.x, e = c * bp + threadIdx.x; r < bp; r += SNT, e += SNT) {
-    if (r / TS <= c / TS) a.US[e] = (r <= c) ? __ldcg(a.F + e) * __ldcg(a.S + c) : 0.0;
+  const int per_cta = ((bp - cta + C - 1) / C) * bp;  // batched as in recon_r2_k: loads before stores
+  for (int base = 0; base < per_cta; base += 16 * SNT) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+      v[u] = (idx < per_cta && r <= c) ? __ldcg(a.F + c * bp + r) * __ldcg(a.S + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = base + u * SNT + threadIdx.x, cc = idx / bp, r = idx - cc * bp, c = cta + cc * C;
+      if (idx < per_cta && r / TS <= c / TS) a.US[c * bp + r] = v[u];
+    }
   }
 }
 
