@@ -32,9 +32,12 @@
 
 namespace cg = cooperative_groups;
 
-// phase timestamps for tools/small_prof.cu (compiled out in the library)
+// phase timestamps for tools/small_prof.cu / tools/chol_bench.cu (compiled out in the library)
 #ifndef SMALL_MARK
 #define SMALL_MARK(id)
+#endif
+#ifndef DSM_MARK
+#define DSM_MARK(cta, id)
 #endif
 
 namespace rutv {
@@ -279,6 +282,128 @@ __device__ __noinline__ void cta_chol_inv(SmallSm& s, int gcol0, int b) {
   for (int jj = 0; jj < 8; ++jj) A[i * LD + j0 + jj] = a[jj];
   __syncthreads();
   if (tid < TS) {  // warp 0: pivots, their reciprocals, breakdown flag, min / max
+    double p = A[tid * LD + tid];
+    const bool ok = (p > 0.0) && isfinite(p);
+    if (!ok) p = 1.0;
+    const double d = sqrt(p);
+    s.piv[tid] = d;
+    s.c[tid] = frcp(d);
+    const bool valid = gcol0 + tid < b;
+    if (valid && !ok) atomicOr(&s.bad, 1);
+    double mn = valid ? d : DBL_MAX, mx = valid ? d : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) {
+      s.dmin = fmin(s.dmin, mn);
+      s.dmax = fmax(s.dmax, mx);
+    }
+  }
+  __syncthreads();
+  const double* rd = s.c;
+  for (int e = tid; e < TS * TS; e += SNT) {
+    const int i = e & 31, j = e >> 5;  // (row i, col j), column-major outputs
+    s.d[j * SLD + i] = (i <= j) ? A[i * LD + j] * rd[i] : 0.0;
+    const double ri = (i <= j) ? A[j * LD + TS + i] * rd[j] : 0.0;  // R^-1(i,j) = L^-1(j,i)/d_j
+    s.di[j * SLD + i] = ri;
+    s.dit[i * SLD + j] = ri;
+  }
+  __syncthreads();
+}
+
+// The same factorisation with 2 x 2 block pivots: 16 double steps instead of 32
+// column steps (one barrier, one reciprocal per two columns).  At double step
+// k (even) every row i > k+1 is updated at once from the current rows k and k+1,
+//   row_i -= [a_ik, a_i,k+1] P^-1 [row_k; row_k+1],  P = [[a_kk, a_k,k+1], [a_k+1,k, a_k+1,k+1]],
+// which in exact arithmetic is column steps k and k+1 (the Schur complement of
+// P is what the two single steps leave); a final pass eliminates a_k+1,k
+// inside each pair (row_k+1 -= a_k+1,k / a_kk row_k), after which the left
+// block is U = D L^T and the right block L^-1 exactly as for cta_chol_inv, and
+// the same epilogue follows.  rb: [2 buffers][2 rows][64] (permuted like
+// rowbuf), cb: [2][2][32] (the pivot columns).  A non-positive / non-finite
+// pivot block is replaced by the identity and flagged from the final pivots.
+__device__ __noinline__ void cta_chol_inv2(SmallSm& s, double* rb, double* cb, int gcol0, int b) {
+  constexpr int LD = 65;
+  double* A = s.aug;
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, g = tid & 7, j0 = g * 8;
+  double a[8];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = j0 + jj;
+    a[jj] = (j < TS) ? s.d[max(i, j) * SLD + min(i, j)] : ((j - TS == i) ? 1.0 : 0.0);
+  }
+  auto pub = [&](int k, int buf) {  // rows k, k+1 and columns k, k+1 for double step k
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (i == k + h) {
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2)
+          *reinterpret_cast<double2*>(&rb[(buf * 2 + h) * 64 + (jj >> 1) * 16 + g * 2]) = make_double2(a[jj], a[jj + 1]);
+      }
+      if (g == (k + h) / 8) cb[(buf * 2 + h) * 32 + i] = a[(k + h) % 8];
+    }
+  };
+  pub(0, 0);
+  __syncthreads();
+#pragma unroll  // (k + h) % 8 must be a compile-time register index
+  for (int k = 0; k < TS; k += 2) {
+    const int buf = (k >> 1) & 1;
+    const double* r0 = rb + (buf * 2 + 0) * 64;
+    const double* r1 = rb + (buf * 2 + 1) * 64;
+    if (i > k + 1) {
+      const double p00 = r0[rb_pos<8>(k)], p01 = r0[rb_pos<8>(k + 1)];
+      const double p10 = r1[rb_pos<8>(k)], p11 = r1[rb_pos<8>(k + 1)];
+      const double x0 = cb[(buf * 2 + 0) * 32 + i], x1 = cb[(buf * 2 + 1) * 32 + i];
+      const double det = fma(p00, p11, -p01 * p10);
+      double c0, c1;
+      if (p00 > 0.0 && det > 0.0 && isfinite(det)) {
+        const double id = frcp(det);
+        c0 = fma(x0, p11, -x1 * p10) * id;
+        c1 = fma(x1, p00, -x0 * p01) * id;
+      } else {
+        c0 = x0;
+        c1 = x1;
+      }
+      double v0[8], v1[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; jj += 2) {
+        const double2 t0 = *reinterpret_cast<const double2*>(&r0[(jj >> 1) * 16 + g * 2]);
+        const double2 t1 = *reinterpret_cast<const double2*>(&r1[(jj >> 1) * 16 + g * 2]);
+        v0[jj] = t0.x; v0[jj + 1] = t0.y;
+        v1[jj] = t1.x; v1[jj + 1] = t1.y;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (j0 + jj > k + 1) a[jj] = fma(-c1, v1[jj], fma(-c0, v0[jj], a[jj]));
+    }
+    if (k + 2 < TS) pub(k + 2, buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) A[i * LD + j0 + jj] = a[jj];
+  __syncthreads();
+  // within each pair: row k+1 -= (a_k+1,k / a_kk) row k, columns > k (both halves)
+  if (i & 1) {
+    const int k = i - 1;
+    double pk = A[k * LD + k];
+    if (!(pk > 0.0) || !isfinite(pk)) pk = 1.0;  // flagged from the stored pivot below
+    const double l = A[i * LD + k] * frcp(pk);
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = j0 + jj;
+      if (j > k) a[jj] = fma(-l, A[k * LD + j], a[jj]);
+    }
+  }
+  __syncthreads();
+  if (i & 1) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) A[i * LD + j0 + jj] = a[jj];
+  }
+  __syncthreads();
+  if (tid < TS) {  // warp 0: pivots, their reciprocals, breakdown flag, min / max (as cta_chol_inv)
     double p = A[tid * LD + tid];
     const bool ok = (p > 0.0) && isfinite(p);
     if (!ok) p = 1.0;
@@ -603,6 +728,211 @@ chol_inv_k(SmallDims d, double* __restrict__ W, double* __restrict__ R, double* 
   }
 }
 
+// ---- Cholesky + inverse with the matrix resident in distributed shared memory
+// One cluster of nb = bp/32 CTAs (b <= 256); CTA j owns tile column j: the
+// Gram / R tiles (i, j), i <= j, and the tiles (i, j), i >= j, of E = R^-T (the
+// right half of the elimination on [G | I], which ends as L^-1 = R^-T).  Tiles
+// never leave shared memory until the end; other CTAs' tiles are read through
+// DSMEM.  Instead of one cluster barrier per phase, readiness is tracked per
+// producer with two counters in its shared memory (polled remotely):
+//   diag_done: R_jj, R_jj^-T of CTA j are final;
+//   row_done = p + 1: R(p, j) of CTA j is final.
+// CTA j: for p < j: R(p, j) = R_pp^-T G(p, j) (R_pp^-T read from CTA p), publish,
+// then G(i, j) -= R(p, i)^T R(p, j) for p < i <= j (R(p, i) read from CTA i) --
+// the diagonal tile first; then factor its own diagonal tile (cta_chol_inv) and
+// publish; then its column of E: for p >= j, E(p, j) = R_pp^-T E(p, j) and
+// E(i, j) -= R(p, i)^T E(p, j) for i > p.  The critical path per block step is
+// the diagonal factorisation plus one flag hop and two 32x32x32 products, with
+// no cluster-wide barrier and no L2 round trip.
+#ifndef RUTV_CHOL_2X2
+#define RUTV_CHOL_2X2 1
+#endif
+constexpr bool kChol2x2 = RUTV_CHOL_2X2;  // 2 x 2 block pivots in the diagonal tiles (cta_chol_inv2)
+
+struct CholDsm {
+  double t[9][TSZ];            // column j: G/R tiles i = 0..j at t[i]; E tiles i = j..nb-1 at t[i + 1]
+  double rb[2 * 2 * 64];       // pivot rows of cta_chol_inv2 (double-buffered pairs)
+  double cb[2 * 2 * 32];       // pivot columns
+  volatile int diag_done;
+  volatile int row_done;
+  unsigned long long dmin_bits, dmax_bits;  // cluster-wide min / max of diag R (CTA 0)
+  int bad;                                  // cluster-wide breakdown flag (CTA 0)
+};
+
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
+// wait until *remote >= target (thread 0 spins; the CTA then proceeds)
+__device__ __forceinline__ void wait_flag(const volatile int* remote, int target) {
+  if (threadIdx.x == 0) {
+    while (*remote < target) {
+    }
+    fence_cluster();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void publish(volatile int* flag, int value) {
+  __syncthreads();  // every thread's writes of the tile are done
+  if (threadIdx.x == 0) {
+    fence_cluster();
+    *flag = value;
+  }
+}
+
+// remote (generic, DSMEM) tile -> local tile, optionally transposed
+__device__ __forceinline__ void tile_copy(double* dst, const double* src, bool tr) {
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+    v[u] = src[c * SLD + r];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+    if (tr) dst[r * SLD + c] = v[u];
+    else dst[c * SLD + r] = v[u];
+  }
+}
+
+// t -= acc (the thread's accumulator elements)
+__device__ __forceinline__ void acc_sub_smem(const double (&acc)[2][2], double* t) {
+  acc_each(acc, [&](int r, int c, double v) { t[c * SLD + r] -= v; });
+}
+
+__global__ void __launch_bounds__(SNT, 1)
+chol_inv_dsm_k(SmallDims d, const double* __restrict__ W, double* __restrict__ R, double* __restrict__ Ri,
+               double* __restrict__ stats) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm_raw[];
+  SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
+  CholDsm& q = *reinterpret_cast<CholDsm*>(sm_raw + (sizeof(SmallSm) + 15) / 8 / 2 * 2);
+  const int j = (int)cl.block_rank(), nb = d.nb, bp = d.bp, b = d.b;
+  auto G = [&](int i) { return q.t[i]; };       // tile (i, j), i <= j
+  auto E = [&](int i) { return q.t[i + 1]; };   // tile (i, j), i >= j
+  auto remote = [&](int rank) { return cl.map_shared_rank(&q, rank); };
+  // ---- load column j of the Gram (identity padding beyond b), E(:, j) = [0; I; 0]
+  if (threadIdx.x == 0) {
+    q.diag_done = 0;
+    q.row_done = 0;
+    q.bad = 0;
+    q.dmin_bits = __double_as_longlong(DBL_MAX);
+    q.dmax_bits = 0ull;
+  }
+  init_stats(s);
+  for (int i = 0; i <= j; ++i) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5, gr = i * TS + r, gc = j * TS + c;
+      v[u] = (gr < b && gc < b) ? __ldcg(W + gr + size_t(gc) * bp) : (gr == gc ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+      G(i)[c * SLD + r] = v[u];
+    }
+  }
+  for (int i = j; i < nb; ++i)
+    for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+      const int r = e & 31, c = e >> 5;
+      E(i)[c * SLD + r] = (i == j && r == c) ? 1.0 : 0.0;
+    }
+  cl.sync();  // every CTA's flags are initialised before anyone polls them
+  DSM_MARK(j, 0);
+  double acc[2][2];
+  // ---- Cholesky steps p < j on column j
+  for (int p = 0; p < j; ++p) {
+    CholDsm* rp = remote(p);
+    wait_flag(&rp->diag_done, 1);
+    tile_copy(s.a, cl.map_shared_rank(s.dit, p), false);  // R_pp^-T
+    __syncthreads();
+    acc_zero(acc);
+    tile_mma(acc, s.a, G(p));
+    __syncthreads();
+    acc_each(acc, [&](int r, int c, double v) { G(p)[c * SLD + r] = v; });  // R(p, j)
+    publish(&q.row_done, p + 1);
+    __syncthreads();
+    // trailing update of column j, the diagonal tile (needed soonest by this CTA) first
+    for (int ii = 0; ii < j - p; ++ii) {
+      const int i = (ii == 0) ? j : p + ii;
+      if (i == j) {
+        tile_copy(s.b, G(p), true);  // R(p, j)^T
+      } else {
+        CholDsm* ri = remote(i);
+        wait_flag(&ri->row_done, p + 1);
+        tile_copy(s.b, ri->t[p], true);  // R(p, i)^T
+      }
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, s.b, G(p));
+      acc_sub_smem(acc, G(i));
+      __syncthreads();
+    }
+  }
+  // ---- diagonal tile j
+  DSM_MARK(j, 1);
+  for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+    const int r = e & 31, c = e >> 5;
+    s.d[c * SLD + r] = G(j)[c * SLD + r];
+  }
+  __syncthreads();
+  if (kChol2x2) cta_chol_inv2(s, q.rb, q.cb, j * TS, b);  // s.d = R_jj, s.di = R_jj^-1, s.dit = R_jj^-T
+  else cta_chol_inv(s, j * TS, b);
+  DSM_MARK(j, 2);
+  for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+    const int r = e & 31, c = e >> 5;
+    G(j)[c * SLD + r] = s.d[c * SLD + r];
+    E(j)[c * SLD + r] = s.dit[c * SLD + r];  // E(j, j) = R_jj^-T I
+  }
+  publish(&q.diag_done, 1);
+  if (threadIdx.x == 0) {  // stats into CTA 0 (non-negative doubles order like their bits)
+    CholDsm* r0 = remote(0);
+    if (s.bad) atomicOr(&r0->bad, 1);
+    atomicMin(&r0->dmin_bits, (unsigned long long)__double_as_longlong(s.dmin));
+    atomicMax(&r0->dmax_bits, (unsigned long long)__double_as_longlong(s.dmax));
+  }
+  // ---- column j of E = R^-T: steps p >= j
+  for (int p = j; p < nb; ++p) {
+    if (p > j) {
+      CholDsm* rp = remote(p);
+      wait_flag(&rp->diag_done, 1);
+      tile_copy(s.a, cl.map_shared_rank(s.dit, p), false);  // R_pp^-T
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, s.a, E(p));
+      __syncthreads();
+      acc_each(acc, [&](int r, int c, double v) { E(p)[c * SLD + r] = v; });
+      __syncthreads();
+    }
+    for (int i = p + 1; i < nb; ++i) {  // E(i, j) -= R(p, i)^T E(p, j)
+      CholDsm* ri = remote(i);
+      wait_flag(&ri->row_done, p + 1);
+      tile_copy(s.b, ri->t[p], true);
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, s.b, E(p));
+      acc_sub_smem(acc, E(i));
+      __syncthreads();
+    }
+  }
+  DSM_MARK(j, 3);
+  // ---- outputs: R column j (zeros below the diagonal tile), Ri row block j = E(:, j)^T
+  for (int i = 0; i < nb; ++i)
+    for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+      const int r = e & 31, c = e >> 5;
+      R[(i * TS + r) + size_t(j * TS + c) * bp] = (i <= j) ? G(i)[c * SLD + r] : 0.0;
+      Ri[(j * TS + r) + size_t(i * TS + c) * bp] = (i >= j) ? E(i)[r * SLD + c] : 0.0;
+    }
+  cl.sync();  // no CTA exits while another may still read its shared memory
+  DSM_MARK(j, 4);
+  if (j == 0 && threadIdx.x == 0) {
+    stats[0] = q.bad ? 1.0 : 0.0;
+    stats[1] = __longlong_as_double((long long)q.dmin_bits);
+    stats[2] = __longlong_as_double((long long)q.dmax_bits);
+  }
+}
+
 struct ReconArgs {
   SmallDims d;
   double* W2;        // Gram of Q1 (b x b valid, ld bp), destroyed
@@ -770,6 +1100,27 @@ __global__ void put_unit_lower_k(int b, const double* __restrict__ F, int bp, do
   }
 }
 
+size_t chol_dsm_smem() { return (sizeof(SmallSm) + 15) / 16 * 16 + sizeof(CholDsm); }
+
+template <class K, class... Args>
+void launch_cluster_smem(K kern, cudaStream_t st, int C, size_t smem, Args... args) {
+  static SmemAttrPerDevice attr;
+  attr.ensure(kern, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(SNT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <class K, class... Args>
 void launch_cluster(K kern, cudaStream_t st, int C, Args... args) {
   // one attribute call per kernel (several kernels share the type K)
@@ -833,7 +1184,12 @@ void small_chol_inv(cudaStream_t st, int64_t b, const SmallWork& w) {
   SmallDims d{(int)b, w.bp, w.bp / TS};
   ProfScope _p(st, C_QR_SMALL, 0.0);
   count_launch(C_QR_SMALL);
-  launch_cluster(chol_inv_k, st, SC, d, w.W1, w.R1, w.R1i, w.stats);
+  static const bool legacy = getenv("RANDUTV_CHOL_L2") != nullptr;  // experiment: the L2-resident kernel
+  if (d.nb <= 8 && !legacy) {
+    launch_cluster_smem(chol_inv_dsm_k, st, d.nb, chol_dsm_smem(), d, (const double*)w.W1, w.R1, w.R1i, w.stats);
+  } else {
+    launch_cluster(chol_inv_k, st, SC, d, w.W1, w.R1, w.R1i, w.stats);
+  }
 }
 
 void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q1, int64_t ldq, double* R,
