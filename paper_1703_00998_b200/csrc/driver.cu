@@ -349,12 +349,13 @@ GraphEntry& graph_entry(const GraphKey& k) {
 // The factorization proper (device pointers only).
 constexpr int kRetry = 1000;  // factor_device: an optimistic CholeskyQR decision failed, redo synchronously
 
-// on_final(c): enqueued work on the factorization's stream has made columns
+// on_final(c, st): work enqueued on the factorization's (internal) stream st has made columns
 // 0..c-1 of T final (used to overlap the D2H of host-staged calls).
 int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
                   uint64_t seed, int64_t k_stop, double* U, double* T, double* V, randutv_info* info,
                   void* ws, size_t ws_bytes, bool optimistic,
-                  const std::function<void(int64_t)>& on_final = std::function<void(int64_t)>()) {
+                  const std::function<void(int64_t, cudaStream_t)>& on_final =
+                      std::function<void(int64_t, cudaStream_t)>()) {
   cudaStream_t ust = o.stream ? (cudaStream_t)o.stream : cudaStreamPerThread;  // the caller's stream
   cudaStream_t st = crit_stream();
   {
@@ -459,6 +460,11 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     chunks.push_back({s0, active.s1, done});
     active.on = false;
   };
+  // (Measured alternative, kept out: beginning every step's SVD right after its
+  // R11 and sweeping a rolling range of the last 12 -- the tail is bounded by
+  // the LAST step's SVD either way (~16 sweeps of one matrix after the loop),
+  // and with a single fold chunk at the end the folds were exposed: c3 251.9 ->
+  // 254.6 ms.)
   auto svd_sweep_here = [&]() {  // one sweep of the active chunk, starting at this point of st
     if (!active.on) return;
     cudaEvent_t e = overlap_event(4 + 1);
@@ -759,7 +765,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
         if (on_final && folded < chunks.size()) {  // a chunk that ended at least one chunk ago
           ensure_lu();
           fold_chunk(chunks[folded]);
-          if (on_final) on_final(b * chunks[folded].s1);
+          if (on_final) on_final(b * chunks[folded].s1, st);
           ++folded;
         }
         launch_svd_chunk();
@@ -1134,15 +1140,15 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     int64_t copied = 0;
     cudaStream_t cps = nullptr;
     cudaEvent_t cev = nullptr;
-    std::function<void(int64_t)> on_final;
+    std::function<void(int64_t, cudaStream_t)> on_final;
     cudaPointerAttributes tat;
     if (!U && opt && cudaPointerGetAttributes(&tat, T) == cudaSuccess && tat.type == cudaMemoryTypeHost) {
       cps = side_stream(2);
       RUTV_CK(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming));
-      on_final = [&](int64_t cols) {
+      on_final = [&](int64_t cols, cudaStream_t fst) {  // fst: the stream the factorization enqueues on
         cols = std::min(cols, n);
         if (cols <= copied) return;
-        RUTV_CK(cudaEventRecord(cev, st));
+        RUTV_CK(cudaEventRecord(cev, fst));
         RUTV_CK(cudaStreamWaitEvent(cps, cev, 0));
         RUTV_CK(cudaMemcpyAsync(T + size_t(copied) * m, dT + size_t(copied) * m, sizeof(double) * m * (cols - copied),
                                 cudaMemcpyDeviceToHost, cps));

@@ -31,12 +31,33 @@ struct JacobiDesc {
   int k, kb, nb;  // matrix order, block width, number of blocks (even)
 };
 
-__global__ void jacobi_init_k(int batch, int k, const double* __restrict__ R, int64_t ldr, int64_t strideR,
-                              double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts) {
+// Workspace layout: one slot per matrix, [B (k^2) | W (k^2) | rotation counts
+// per sweep (MAX_SWEEPS + 1 ints), next-sweep index (1 int)] padded to
+// jslot(k) = jacobi_work_elems(1, k) doubles; matrix mat of a launch whose
+// work pointer is ``work`` sits at work + mat jslot(k).  A range of matrices
+// [s0, s1) of a larger workspace is therefore itself a valid batch at
+// work + s0 jslot(k), whatever batch sizes began / advanced / finish it (the
+// incremental SVDs of the driver begin one matrix per step and sweep ranges).
+__host__ __device__ __forceinline__ int64_t jslot(int k) { return 2 * int64_t(k) * k + (MAX_SWEEPS + 2); }
+struct JSlot {
+  double* B;
+  double* W;
+  int* cnt;   // cnt[s]: rotations in sweep s - 1 (cnt[0] = 1)
+  int* next;  // next sweep to run, -1 once converged
+};
+__device__ __forceinline__ JSlot jslot_of(double* work, int k, int mat) {
+  double* B = work + int64_t(mat) * jslot(k);
+  int* cnt = reinterpret_cast<int*>(B + 2 * int64_t(k) * k);
+  return {B, B + int64_t(k) * k, cnt, cnt + MAX_SWEEPS + 1};
+}
+
+__global__ void jacobi_init_k(int k, const double* __restrict__ R, int64_t ldr, int64_t strideR,
+                              double* __restrict__ work) {
   const int mat = blockIdx.y;
   const double* Ri = R + int64_t(mat) * strideR;
-  double* B = Bw + int64_t(mat) * k * k;
-  double* W = Wm + int64_t(mat) * k * k;
+  const JSlot js = jslot_of(work, k, mat);
+  double* B = js.B;
+  double* W = js.W;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < int64_t(k) * k;
        idx += int64_t(gridDim.x) * blockDim.x) {
     int r = int(idx % k), c = int(idx / k);
@@ -44,8 +65,8 @@ __global__ void jacobi_init_k(int batch, int k, const double* __restrict__ R, in
     W[idx] = (r == c) ? 1.0 : 0.0;
   }
   if (blockIdx.x == 0) {
-    for (int s = threadIdx.x; s <= MAX_SWEEPS; s += blockDim.x) counts[mat * (MAX_SWEEPS + 1) + s] = (s == 0);
-    if (threadIdx.x == 0) counts[batch * (MAX_SWEEPS + 1) + mat] = 0;  // next sweep (-1: converged)
+    for (int s = threadIdx.x; s <= MAX_SWEEPS; s += blockDim.x) js.cnt[s] = (s == 0);
+    if (threadIdx.x == 0) *js.next = 0;  // next sweep (-1: converged)
   }
 }
 
@@ -190,18 +211,18 @@ __device__ void store_pair(const double* sB, const double* sW, double* B, double
 // One block-pair operation for tournament round ``round`` of sweep ``sweep``
 // (one launch per round; used when a matrix's blocks do not fit one cluster).
 __global__ void __launch_bounds__(JNT)
-jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ Bw, double* __restrict__ Wm,
-               int* __restrict__ counts, double tol) {
+jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ work, double tol) {
   extern __shared__ __align__(16) double js[];
   __shared__ double nrm[64];
   const int mat = blockIdx.y;
-  int* cnt = counts + mat * (MAX_SWEEPS + 1);
+  const JSlot slot = jslot_of(work, d.k, mat);
+  int* cnt = slot.cnt;
   if (cnt[sweep] == 0) return;  // previous sweep did no rotation: converged
   const int k = d.k, kb = d.kb;
   int bp, bq;
   rr_pair(d.nb, round, blockIdx.x, bp, bq);
-  double* B = Bw + int64_t(mat) * k * k;
-  double* W = Wm + int64_t(mat) * k * k;
+  double* B = slot.B;
+  double* W = slot.W;
   double* sB = js;
   double* sW = js + size_t(2 * kb) * k;
   load_pair(sB, sW, B, W, k, kb, bp, bq);
@@ -216,18 +237,18 @@ jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ Bw, doub
 // cluster barrier between rounds (columns move between CTAs through L2) and a
 // cluster-wide rotation count deciding convergence.
 __global__ void __launch_bounds__(JNT)
-jacobi_cluster_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts,
-                 double tol) {
+jacobi_cluster_k(JacobiDesc d, double* __restrict__ work, double tol) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double js[];
   __shared__ double nrm[64];
   __shared__ int rot_sm;
   const int mat = blockIdx.y;
   const int cta = (int)cluster.block_rank();
-  int* cnt = counts + mat * (MAX_SWEEPS + 1);
+  const JSlot slot = jslot_of(work, d.k, mat);
+  int* cnt = slot.cnt;
   const int k = d.k, kb = d.kb;
-  double* B = Bw + int64_t(mat) * k * k;
-  double* W = Wm + int64_t(mat) * k * k;
+  double* B = slot.B;
+  double* W = slot.W;
   double* sB = js;
   double* sW = js + size_t(2 * kb) * k;
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
@@ -355,8 +376,7 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
 
 template <int EPL>
 __global__ void __launch_bounds__(JNT)
-jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm, int* __restrict__ counts,
-                  double tol, int max_sweeps) {
+jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_sweeps) {
   constexpr int KB = 16, KP = 32 * EPL;  // block width, padded column length
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double js[];
@@ -366,10 +386,11 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
   const int mat = blockIdx.y;
   const int cta = (int)cluster.block_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* cnt = counts + mat * (MAX_SWEEPS + 1);
+  const JSlot slot = jslot_of(work, d.k, mat);
+  int* cnt = slot.cnt;
   const int k = d.k;
-  double* B = Bw + int64_t(mat) * k * k;
-  double* W = Wm + int64_t(mat) * k * k;
+  double* B = slot.B;
+  double* W = slot.W;
   // global <-> shared for one block (16 columns, zero padding beyond k)
   // (16-byte accesses when k is even: a column pair of rows r, r+1 is aligned)
   const bool vec = (k & 1) == 0;
@@ -417,8 +438,8 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
     }
   };
   // resumable: up to max_sweeps sweeps from the stored next-sweep index
-  // (counts[batch (MAX_SWEEPS + 1) + mat], -1 once a sweep made no rotation)
-  int* next = counts + int(gridDim.y) * (MAX_SWEEPS + 1) + mat;
+  // (-1 once a sweep made no rotation)
+  int* next = slot.next;
   const int s0 = __ldcg(next);
   if (s0 < 0) return;
   const int s1 = min(MAX_SWEEPS, s0 + max_sweeps);
@@ -504,15 +525,16 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ Bw, double* __restrict__ Wm
 
 // sigma_j = ||B(:,j)||, sort descending, Us = W(:,perm), Vs = B(:,perm) / sigma.
 __global__ void __launch_bounds__(JNT)
-jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict__ Wm, double* __restrict__ D,
-                  double* __restrict__ Us, double* __restrict__ Vs, const int* __restrict__ counts,
-                  int* __restrict__ sweeps_out) {
+jacobi_finalize_k(int k, double* __restrict__ work, double* __restrict__ D, double* __restrict__ Us,
+                  double* __restrict__ Vs, int* __restrict__ sweeps_out) {
   extern __shared__ __align__(16) double fs[];
   double* sig = fs;                           // k
   int* rank = reinterpret_cast<int*>(fs + k);  // k
   const int mat = blockIdx.x;
-  const double* B = Bw + int64_t(mat) * k * k;
-  const double* W = Wm + int64_t(mat) * k * k;
+  const JSlot slot = jslot_of(work, k, mat);
+  const double* B = slot.B;
+  const double* W = slot.W;
+  const int* cnt = slot.cnt;
   double* Di = D + int64_t(mat) * k;
   double* Ui = Us + int64_t(mat) * k * k;
   double* Vi = Vs + int64_t(mat) * k * k;
@@ -547,7 +569,7 @@ jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict
   if (nz == 0) {
     if (threadIdx.x == 0 && sweeps_out) {
       int s = 0;
-      while (s < MAX_SWEEPS && counts[mat * (MAX_SWEEPS + 1) + s + 1] > 0) ++s;
+      while (s < MAX_SWEEPS && cnt[s + 1] > 0) ++s;
       sweeps_out[mat] = s + 1;
     }
     return;
@@ -592,7 +614,7 @@ jacobi_finalize_k(int k, const double* __restrict__ Bw, const double* __restrict
   }
   if (threadIdx.x == 0 && sweeps_out) {
     int s = 0;
-    while (s < MAX_SWEEPS && counts[mat * (MAX_SWEEPS + 1) + s + 1] > 0) ++s;
+    while (s < MAX_SWEEPS && cnt[s + 1] > 0) ++s;
     sweeps_out[mat] = s + 1;
   }
 }
@@ -626,14 +648,14 @@ bool jacobi_single_launch(int k) {
 
 // per matrix: B and W (k x k each) and MAX_SWEEPS + 2 int slots (sweep counts,
 // next-sweep index) padded to MAX_SWEEPS + 2 doubles -- an even count, so that
-// jacobi_work_elems(j0, k) is a 16-byte aligned offset for any j0 (callers
-// carve sub-batches starting at matrix j0; the k-even block I/O is 16-byte)
+// jacobi_work_elems(j0, k) = j0 jslot(k) is a 16-byte aligned offset for any j0
+// (callers carve sub-batches starting at matrix j0; the k-even block I/O is 16-byte)
 static_assert((MAX_SWEEPS + 2) % 2 == 0, "16-byte aligned sub-batch offsets");
-size_t jacobi_work_elems(int batch, int k) { return size_t(2) * batch * k * k + size_t(batch) * (MAX_SWEEPS + 2); }
+size_t jacobi_work_elems(int batch, int k) { return size_t(batch) * size_t(jslot(k)); }
 
 namespace {
 // up to max_sweeps sweeps of jacobi_cluster2_k on every matrix of the batch
-void launch_c2(cudaStream_t st, int batch, int k, double* Bw, double* Wm, int* counts, int max_sweeps) {
+void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) {
   JacobiDesc d = make_desc(k);
   const int csize = d.nb / 2;
   const double tol = double(k) * DBL_EPSILON;
@@ -657,39 +679,23 @@ void launch_c2(cudaStream_t st, int batch, int k, double* Bw, double* Wm, int* c
   cfg.numAttrs = 1;
   ProfScope _p(st, K_SVD, 0.0);
   count_launch(K_SVD);
-  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, Bw, Wm, counts, tol, max_sweeps));
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, work, tol, max_sweeps));
 }
 
-struct JacobiBufs {
-  double *Bw, *Wm;
-  int* counts;
-};
-JacobiBufs jacobi_bufs(double* work, int batch, int k) {
-  return {work, work + size_t(batch) * k * k, reinterpret_cast<int*>(work + size_t(2) * batch * k * k)};
-}
-void launch_init(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
-                 const JacobiBufs& jb) {
+void launch_init(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR, double* work) {
   dim3 g((unsigned)std::min<int64_t>(cdiv(int64_t(k) * k, 256), 64), batch);
   ProfScope _p(st, K_SVD, 0.0);
   count_launch(K_SVD);
-  jacobi_init_k<<<g, 256, 0, st>>>(batch, k, R, ldr, strideR, jb.Bw, jb.Wm, jb.counts);
+  jacobi_init_k<<<g, 256, 0, st>>>(k, R, ldr, strideR, work);
   RUTV_LAUNCH_CK();
 }
-void launch_finalize(cudaStream_t st, int batch, int k, const JacobiBufs& jb, double* D, double* Us, double* Vs,
-                     int* sweeps_out);
-}  // namespace
 
-
-namespace {
-void launch_finalize(cudaStream_t st, int batch, int k, const JacobiBufs& jb, double* D, double* Us, double* Vs,
+void launch_finalize(cudaStream_t st, int batch, int k, double* work, double* D, double* Us, double* Vs,
                      int* sweeps_out) {
-  double* Bw = jb.Bw;
-  double* Wm = jb.Wm;
-  int* counts = jb.counts;
   const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
   static SmemAttrPerDevice attr_f;
   if (fsmem > 48 * 1024) attr_f.ensure(jacobi_finalize_k, fsmem);
-  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, Bw, Wm, D, Us, Vs, counts, sweeps_out); }
+  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, work, D, Us, Vs, sweeps_out); }
   RUTV_LAUNCH_CK();
 }
 }  // namespace
@@ -698,38 +704,29 @@ bool jacobi_incremental(int k) { return k > 1 && k <= 256 && make_desc(k).kb == 
 
 void jacobi_begin(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR, double* work) {
   if (batch <= 0) return;
-  launch_init(st, batch, k, R, ldr, strideR, jacobi_bufs(work, batch, k));
+  launch_init(st, batch, k, R, ldr, strideR, work);
 }
 void jacobi_sweeps(cudaStream_t st, int batch, int k, double* work, int nsweeps) {
   if (batch <= 0) return;
-  JacobiBufs jb = jacobi_bufs(work, batch, k);
-  launch_c2(st, batch, k, jb.Bw, jb.Wm, jb.counts, nsweeps);
+  launch_c2(st, batch, k, work, nsweeps);
 }
 void jacobi_end(cudaStream_t st, int batch, int k, double* work, double* D, double* Us, double* Vs,
                 int* sweeps_out) {
   if (batch <= 0) return;
-  JacobiBufs jb = jacobi_bufs(work, batch, k);
-  launch_c2(st, batch, k, jb.Bw, jb.Wm, jb.counts, MAX_SWEEPS);  // the remaining sweeps, if any
-  launch_finalize(st, batch, k, jb, D, Us, Vs, sweeps_out);
+  launch_c2(st, batch, k, work, MAX_SWEEPS);  // the remaining sweeps, if any
+  launch_finalize(st, batch, k, work, D, Us, Vs, sweeps_out);
 }
 
 void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR,
                         double* D, double* Us, double* Vs, double* work, int* sweeps_out) {
   if (batch <= 0 || k <= 0) return;
   JacobiDesc d = make_desc(k);
-  double* Bw = work;
-  double* Wm = work + size_t(batch) * k * k;
-  int* counts = reinterpret_cast<int*>(work + size_t(2) * batch * k * k);
-  {
-    dim3 g((unsigned)std::min<int64_t>(cdiv(int64_t(k) * k, 256), 64), batch);
-    { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_init_k<<<g, 256, 0, st>>>(batch, k, R, ldr, strideR, Bw, Wm, counts); }
-    RUTV_LAUNCH_CK();
-  }
+  launch_init(st, batch, k, R, ldr, strideR, work);
   const size_t smem = size_t(2) * 2 * d.kb * k * sizeof(double);
   const double tol = double(k) * DBL_EPSILON;
   const int csize = d.nb / 2;
   if (jacobi_incremental(k)) {
-    launch_c2(st, batch, k, Bw, Wm, counts, MAX_SWEEPS);
+    launch_c2(st, batch, k, work, MAX_SWEEPS);
   } else if (k > 1 && csize <= MAX_CLUSTER) {
 
     // one cluster per matrix runs every round and sweep in-kernel
@@ -749,7 +746,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
     cfg.numAttrs = 1;
     ProfScope _p(st, K_SVD, 0.0);
     count_launch(K_SVD);
-    RUTV_CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_k, d, Bw, Wm, counts, tol));
+    RUTV_CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_k, d, work, tol));
   } else if (k > 1) {
     static SmemAttrPerDevice attr_r;
     if (smem > 48 * 1024) attr_r.ensure(jacobi_round_k, smem);
@@ -763,11 +760,14 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
       for (; sweep < end; ++sweep) {
         for (int round = 0; round < d.nb - 1; ++round) {
           dim3 g(d.nb / 2, batch);
-          { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_round_k<<<g, JNT, smem, st>>>(d, sweep, round, Bw, Wm, counts, tol); }
+          { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_round_k<<<g, JNT, smem, st>>>(d, sweep, round, work, tol); }
           RUTV_LAUNCH_CK();
         }
       }
-      RUTV_CK(cudaMemcpyAsync(h.data(), counts, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, st));
+      // the rotation counts of every matrix: MAX_SWEEPS + 1 ints at the end of each slot
+      RUTV_CK(cudaMemcpy2DAsync(h.data(), sizeof(int) * (MAX_SWEEPS + 1), work + 2 * int64_t(k) * k,
+                                sizeof(double) * size_t(jslot(k)), sizeof(int) * (MAX_SWEEPS + 1), batch,
+                                cudaMemcpyDeviceToHost, st));
       RUTV_CK(cudaStreamSynchronize(st));
       bool all = true;
       for (int b = 0; b < batch; ++b) all &= (h[size_t(b) * (MAX_SWEEPS + 1) + sweep] == 0);
@@ -775,7 +775,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
       chunk = 2;
     }
   }
-  launch_finalize(st, batch, k, JacobiBufs{Bw, Wm, counts}, D, Us, Vs, sweeps_out);
+  launch_finalize(st, batch, k, work, D, Us, Vs, sweeps_out);
 }
 
 }  // namespace rutv

@@ -215,3 +215,25 @@ def test_graph_replay_bitwise(uv, name, scale):
     ref = oracle.randutv(c.A, min(c.b, m, n), c.q, c.seed, build_ortho=False)
     par = check_parity(to_host(outs[-1][0]), ref["T"], ref["a_fro"])
     assert par["diag_ok"] and par["ek_ok"], par
+
+
+@pytest.mark.parametrize("m,n,b,q", [(3000, 3000, 64, 1), (2600, 2000, 128, 2)])
+def test_pinned_host_copy_back_ordering(m, n, b, q):
+    """Host-staged calls copy T's finished column blocks back while the loop
+    runs; the copies must be ordered after the folds on the factorization's
+    internal stream (a copy ordered on the caller's stream raced with them and
+    returned undiagonalised blocks).  Every b x b diagonal block diagonal and
+    equal to the device path's to rounding."""
+    A = testmat.gaussian(m, n, m + n + b)
+    Ah = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory()
+    Th = torch.empty(n, m, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        rc = P.factor_raw(m, n, Ah.data_ptr(), m, b, q, 9, 0, None, Th.data_ptr(), None)
+        assert rc == 0
+        _, Td, _, _ = P.randutv(to_dev(A), b, q, 9, with_uv=False)
+        torch.cuda.synchronize()
+        Tp, Td = Th.t().numpy(), to_host(Td)
+        k = min(m, n)
+        assert diag_blocks_ok(Tp[:k, :k], b, k)
+        assert np.array_equal(Tp == 0.0, Td == 0.0)
+        assert np.abs(Tp - Td).max() <= 1e-12 * np.linalg.norm(A)
