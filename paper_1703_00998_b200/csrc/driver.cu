@@ -114,6 +114,7 @@ struct Work {
   double *G, *Y, *Y2, *P, *P2, *Vu, *Wt, *Wt2, *tau, *Rtmp, *Ttmp;
   double *WG, *H;  // look-ahead sketch: [W_u | G'] (m x (b + bs)), H = W_u^T G' (b x bs)
   double *Pbig, *part2;  // P_big = T(:, J3) Q1(b:, :) (m x b) and its split-K scratch (side stream)
+  double *LT, *MT;       // L T_v, M T_v (b x b): the P2 assembly's right factors (read on two streams)
   size_t part2_elems;
   double *Qo, *Ro, *Do, *Uso, *Vso, *jworko;  // over-sampling: thin Q, R, SVD of R (width b + p)
   double *Tv, *Tu, *Rall, *Dall, *Usall, *Vsall, *jwork;
@@ -152,6 +153,8 @@ Work carve(Arena& ar, const Plan& p) {
   w.P = ar.take<double>(size_t(m) * b);
   w.P2 = ar.take<double>(size_t(m) * b);
   w.Pbig = ar.take<double>(size_t(m) * b);
+  w.LT = ar.take<double>(size_t(b) * b);
+  w.MT = ar.take<double>(size_t(b) * b);
   w.part2_elems = size_t(8) * m * b + size_t(148) * 32 * 1024;
   w.part2 = ar.take<double>(w.part2_elems);
   w.Vu = w.WG;  // W_u (T-only mode) in the first b columns of [W_u | G']
@@ -630,16 +633,26 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
             RUTV_CK(cudaEventRecord(ev_yflags, st));
           }
           // P2 = P T_v = T(:, J2) (L T_v) - P_big (M T_v): two b x b products
-          // replace one m x b x b pass
+          // replace one m x b x b pass.  Only the trailing rows r0:m are on the
+          // critical path (the panel update and QR need them); the rows above
+          // (I1, needed only by their own rank-b update) are formed on the side
+          // stream, ahead of that update -- in the late steps r0 >> m_i.
           set_gemm_role(C_GEMM_RIGHT);
           int64_t ldm = 0;
           const double* M = panel_qr_M(qwy, b, &ldm);
-          dg(w, st, false, false, b, b, b, 1.0, Wv, ldwv, Tv, b, 0.0, w.Ttmp, b);        // L T_v
-          dg(w, st, false, false, b, b, b, 1.0, M, ldm, Tv, b, 0.0, w.H, b);             // M T_v
+          dg(w, st, false, false, b, b, b, 1.0, Wv, ldwv, Tv, b, 0.0, w.LT, b);          // L T_v
+          dg(w, st, false, false, b, b, b, 1.0, M, ldm, Tv, b, 0.0, w.MT, b);            // M T_v
+          if (r0 > 0) {  // rows I1 on the side stream (after P_big there, stream order)
+            cudaEvent_t f1 = overlap_event(10);
+            RUTV_CK(cudaEventRecord(f1, st));
+            RUTV_CK(cudaStreamWaitEvent(upd, f1, 0));
+            dgemm(upd, false, false, r0, b, b, 1.0, TJ, m, w.LT, b, 0.0, w.P2, m, nullptr, 0);
+            dgemm(upd, false, false, r0, b, b, -1.0, w.Pbig, m, w.MT, b, 1.0, w.P2, m, nullptr, 0);
+          }
           ensure_lu();
-          dg(w, st, false, false, m, b, b, 1.0, TJ, m, w.Ttmp, b, 0.0, w.P2, m);         // T(:, J2) L T_v
+          dg(w, st, false, false, mi, b, b, 1.0, TJ + r0, m, w.LT, b, 0.0, w.P2 + r0, m);          // T(r0:, J2) L T_v
           RUTV_CK(cudaStreamWaitEvent(st, j, 0));
-          dg(w, st, false, false, m, b, b, -1.0, w.Pbig, m, w.H, b, 1.0, w.P2, m);       // - P_big M T_v
+          dg(w, st, false, false, mi, b, b, -1.0, w.Pbig + r0, m, w.MT, b, 1.0, w.P2 + r0, m);   // - P_big M T_v
         } else {
           check_qr(panel_qr(st, ni, b, Wv, ldwv, w.Rtmp, b, w.tau, Tv, b, qwy));
           if (copy_flags && *qwy.flag_count > 0) {

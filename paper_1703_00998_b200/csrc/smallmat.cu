@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 #ifndef DSM_MARK
 #define DSM_MARK(cta, id)
 #endif
+#ifndef LU_MARK
+#define LU_MARK(cta, id)
+#endif
 
 namespace rutv {
 
@@ -442,7 +445,8 @@ __device__ __noinline__ void cta_chol_inv2(SmallSm& s, double* rb, double* cb, i
 // they become final, giving E' with E' U~^T = diag(piv), so U~^-1 = E'^T diag(piv)^-1.
 // In: F tile (column-major in s.d).  Out: s.d = L (strict lower) \ U~, s.di =
 // L^-1, s.e = U~^-1, s.sgn.
-__device__ __noinline__ void cta_lu_sign_inv(SmallSm& s) {
+template <class SM>
+__device__ __noinline__ void cta_lu_sign_inv(SM& s) {
   constexpr int LD = 97;
   double* A = s.aug;
   const int tid = threadIdx.x;
@@ -933,6 +937,195 @@ chol_inv_dsm_k(SmallDims d, const double* __restrict__ W, double* __restrict__ R
   }
 }
 
+// ---- sign-modified LU with L^-1 and U~^-1, resident in distributed shared
+// memory (the reconstruction's LU, recon_lu_k's outputs), b <= 256: one
+// cluster of nb CTAs, CTA j owns column j of F (becoming L \ U~), column j of
+// E1 = L^-1 and column k2 = nb-1-j of E2 = U~^-T (forward elimination of
+// U~^T; the two E columns of a CTA hold nb + 1 tiles together).  Right-looking
+// at tile level with per-producer counters instead of cluster barriers:
+//   diag_done: CTA j's diagonal tile is factored (s.di = L_jj^-1, s.e = U~_jj^-1);
+//   urow_done = p + 1: U~(p, j) = L_pp^-1 F(p, j) is final in CTA j;
+//   lcol_done = i: L(i', j) = F(i', j) U~_jj^-1 is final for i' <= i.
+// The critical path per block step is the diagonal tile's factorisation plus
+// one flag hop and three 32x32x32 products.
+struct LuSm {
+  double d[TSZ], di[TSZ], e[TSZ];  // the diagonal tile: in F, out L \ U~, L^-1, U~^-1 (cta_lu_sign_inv)
+  double a[TSZ], b[TSZ];           // operand staging
+  double aug[TS * 97];
+  double piv[TS];
+  double sgn[TS];
+  double c[TS];
+  double rowbuf[2][96];
+  double colbuf[2][TS];
+  double f[8][TSZ];     // column j of F
+  double x[9][TSZ];     // E1(i, j), i >= j at x[i - j]; E2(i, k2), i >= k2 at x[nb - j + i - k2]
+  volatile int diag_done, urow_done, lcol_done;
+};
+
+__global__ void __launch_bounds__(SNT, 1)
+lu_dsm_k(SmallDims dd, double* __restrict__ F, double* __restrict__ Li, double* __restrict__ Ui,
+         double* __restrict__ S, double* __restrict__ US) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm_raw[];
+  LuSm& q = *reinterpret_cast<LuSm*>(sm_raw);
+  const int j = (int)cl.block_rank(), nb = dd.nb, bp = dd.bp, k2 = nb - 1 - j;
+  auto E1 = [&](int i) { return q.x[i - j]; };             // i >= j
+  auto E2 = [&](int i) { return q.x[nb - j + i - k2]; };   // i >= k2
+  auto remote = [&](int rank) { return cl.map_shared_rank(&q, rank); };
+  if (threadIdx.x == 0) {
+    q.diag_done = 0;
+    q.urow_done = 0;
+    q.lcol_done = j;
+  }
+  for (int i = 0; i < nb; ++i) {  // column j of F (zero-padded by recon_r2_k), E columns = [0; I; 0]
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+      v[u] = __ldcg(F + (i * TS + r) + size_t(j * TS + c) * bp);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * SNT, r = e & 31, c = e >> 5;
+      q.f[i][c * SLD + r] = v[u];
+    }
+  }
+  for (int t = 0; t <= nb; ++t)
+    for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+      const int r = e & 31, c = e >> 5;
+      q.x[t][c * SLD + r] = ((t == 0 || t == nb - j) && r == c) ? 1.0 : 0.0;  // E1(j, j) = I, E2(k2, k2) = I
+    }
+  cl.sync();
+  LU_MARK(j, 0);
+  double acc[2][2];
+  // E2(p, k2) = U~_pp^-T E2(p, k2);  E2(i, k2) -= U~(p, i)^T E2(p, k2), i > p
+  int e2_next = k2;  // next E2 step of this CTA
+  auto e2_step = [&](int p) {
+    LuSm* rp = remote(p);
+    if (p != j) wait_flag(&rp->diag_done, 1);
+    tile_copy(q.a, rp->e, true);  // U~_pp^-T
+    __syncthreads();
+    acc_zero(acc);
+    tile_mma(acc, q.a, E2(p));
+    __syncthreads();
+    acc_each(acc, [&](int r, int c, double v) { E2(p)[c * SLD + r] = v; });
+    __syncthreads();
+    for (int i = p + 1; i < nb; ++i) {
+      LuSm* ri = remote(i);
+      if (i != j) wait_flag(&ri->urow_done, p + 1);
+      tile_copy(q.b, ri->f[p], true);  // U~(p, i)^T
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, q.b, E2(p));
+      acc_sub_smem(acc, E2(i));
+      __syncthreads();
+    }
+    e2_next = p + 1;
+  };
+  // ---- phase 1: the LU steps p < j on column j
+  for (int p = 0; p < j; ++p) {
+    LuSm* rp = remote(p);
+    wait_flag(&rp->diag_done, 1);
+    tile_copy(q.a, rp->di, false);  // L_pp^-1
+    __syncthreads();
+    acc_zero(acc);
+    tile_mma(acc, q.a, q.f[p]);
+    __syncthreads();
+    acc_each(acc, [&](int r, int c, double v) { q.f[p][c * SLD + r] = v; });  // U~(p, j)
+    publish(&q.urow_done, p + 1);
+    __syncthreads();
+    // F(i, j) -= L(i, p) U~(p, j); at the last step before the diagonal only
+    // the diagonal tile (the rest follows the diagonal factorisation)
+    const int iend = (p == j - 1) ? j + 1 : nb;
+    for (int i = p + 1; i < iend; ++i) {
+      wait_flag(&rp->lcol_done, i);
+      tile_copy(q.b, rp->f[i], false);
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, q.b, q.f[p]);
+      acc_sub_smem(acc, q.f[i]);
+      __syncthreads();
+    }
+    // this CTA waits for the next diagonal anyway: advance its E2 column
+    // (its own U~(p, j) is final; the other columns' are published early)
+    if (p < j - 1 && p >= k2 && e2_next == p) e2_step(p);
+  }
+  // ---- the diagonal tile j, then L(i, j) = F(i, j) U~_jj^-1 for i > j
+  for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+    const int r = e & 31, c = e >> 5;
+    q.d[c * SLD + r] = q.f[j][c * SLD + r];
+  }
+  __syncthreads();
+  cta_lu_sign_inv(q);  // q.d = L_jj \ U~_jj (pivots on the diagonal), q.di = L_jj^-1, q.e = U~_jj^-1, q.sgn
+  for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+    const int r = e & 31, c = e >> 5;
+    q.f[j][c * SLD + r] = q.d[c * SLD + r];
+  }
+  publish(&q.diag_done, 1);
+  LU_MARK(j, 2);
+  __syncthreads();
+  for (int i = j + 1; i < nb; ++i) {
+    if (j > 0) {  // the deferred update of step j - 1 on tile (i, j)
+      LuSm* rp = remote(j - 1);
+      wait_flag(&rp->lcol_done, i);
+      tile_copy(q.b, rp->f[i], false);
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, q.b, q.f[j - 1]);
+      acc_sub_smem(acc, q.f[i]);
+      __syncthreads();
+    }
+    acc_zero(acc);
+    tile_mma(acc, q.f[i], q.e);  // L(i, j) = F(i, j) U~_jj^-1
+    __syncthreads();
+    acc_each(acc, [&](int r, int c, double v) { q.f[i][c * SLD + r] = v; });
+    publish(&q.lcol_done, i);
+    __syncthreads();
+  }
+  LU_MARK(j, 3);
+  // ---- phases 2 and 3: E1 column j (steps p >= j), E2 column k2 (steps p >= k2)
+  for (int p = 0; p < nb; ++p) {
+    if (p >= j) {  // E1(p, j) = L_pp^-1 E1(p, j);  E1(i, j) -= L(i, p) E1(p, j), i > p
+      LuSm* rp = remote(p);
+      if (p > j) {
+        wait_flag(&rp->diag_done, 1);
+        tile_copy(q.a, rp->di, false);
+      } else {
+        tile_copy(q.a, q.di, false);
+      }
+      __syncthreads();
+      acc_zero(acc);
+      tile_mma(acc, q.a, E1(p));
+      __syncthreads();
+      acc_each(acc, [&](int r, int c, double v) { E1(p)[c * SLD + r] = v; });
+      __syncthreads();
+      for (int i = p + 1; i < nb; ++i) {
+        wait_flag(&rp->lcol_done, i);
+        tile_copy(q.b, rp->f[i], false);  // L(i, p)
+        __syncthreads();
+        acc_zero(acc);
+        tile_mma(acc, q.b, E1(p));
+        acc_sub_smem(acc, E1(i));
+        __syncthreads();
+      }
+    }
+    if (p >= e2_next) e2_step(p);
+  }
+  // ---- outputs: F = L \ U~ (column j), Li column j, Ui row block k2 = E2(:, k2)^T, S, US = U~ S
+  if (threadIdx.x < TS) S[j * TS + threadIdx.x] = q.sgn[threadIdx.x];
+  for (int i = 0; i < nb; ++i)
+    for (int e = threadIdx.x; e < TS * TS; e += SNT) {
+      const int r = e & 31, c = e >> 5, gr = i * TS + r, gc = j * TS + c;
+      const double fv = q.f[i][c * SLD + r];
+      F[gr + size_t(gc) * bp] = fv;
+      Li[gr + size_t(gc) * bp] = (i >= j) ? E1(i)[c * SLD + r] : 0.0;
+      US[gr + size_t(gc) * bp] = (gr <= gc) ? fv * q.sgn[c] : 0.0;
+      Ui[(k2 * TS + r) + size_t(i * TS + c) * bp] = (i >= k2) ? E2(i)[r * SLD + c] : 0.0;
+    }
+  cl.sync();  // no CTA exits while another may still read its shared memory
+  LU_MARK(j, 5);
+}
+
 struct ReconArgs {
   SmallDims d;
   double* W2;        // Gram of Q1 (b x b valid, ld bp), destroyed
@@ -1228,7 +1421,11 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
   {
     ProfScope _p(st, C_QR_SMALL, 0.0);
     count_launch(C_QR_SMALL);
-    launch_cluster(recon_lu_k, st, SC, a);
+    static const bool legacy = getenv("RANDUTV_LU_L2") != nullptr;  // experiment: the L2-resident kernel
+    if (a.d.nb <= 8 && !legacy)
+      launch_cluster_smem(lu_dsm_k, st, a.d.nb, sizeof(LuSm), a.d, a.F, a.Li, a.Ui, a.S, a.US);
+    else
+      launch_cluster(recon_lu_k, st, SC, a);
   }
   // M (needed next by W = -Q1(b:) M) stays on st; T_w, tau and R_h are not
   // needed until after the caller's W GEMM, so with a side stream they are
