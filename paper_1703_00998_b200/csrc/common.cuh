@@ -37,6 +37,42 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int kMaxDevices = 64;
 
+// Programmatic dependent launch (PDL).  Every kernel of the library begins
+// with pdl_begin(): it waits until the previous kernel of its stream has
+// completed and its writes are visible (griddepcontrol.wait -- a no-op when
+// the kernel was not launched as a programmatic dependent), then lets the next
+// kernel of the stream be launched (griddepcontrol.launch_dependents, effective
+// once every CTA of this grid has started).  Launched through launch_k with
+// programmatic stream serialisation, a dependent kernel's launch and CTA
+// scheduling overlap the end of its predecessor instead of following its
+// completion -- the per-kernel gap of the latency-bound chains.  Nothing runs
+// before the wait, so ordering and visibility are those of plain stream order.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_on();         // false with RANDUTV_NO_PDL set (prof.cu)
+long long pdl_max_ctas();  // largest grid launched as a programmatic dependent (prof.cu)
+
+template <class K, class... Args>
+void launch_k(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // only grids of at most one wave: a dependent grid's CTAs are scheduled
+  // early and wait, and a many-wave grid would hold SMs that the side streams'
+  // GEMMs use meanwhile (c3 251.6 -> 257.1 ms with PDL on every launch)
+  const long long ctas = (long long)grid.x * grid.y * grid.z;
+  cfg.numAttrs = (pdl_on() && ctas <= pdl_max_ctas()) ? 1 : 0;
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 inline int current_device() {
   int d = 0;
   RUTV_CK(cudaGetDevice(&d));

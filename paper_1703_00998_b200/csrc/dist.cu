@@ -88,13 +88,14 @@ struct Comm {
 
 namespace {
 __global__ void add_k(size_t n, const double* __restrict__ s, double* __restrict__ d) {
+  pdl_begin();
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     d[i] += s[i];
 }
 void add_into(cudaStream_t st, size_t n, const double* s, double* d) {
   if (n == 0) return;
   const int blocks = (int)std::min<size_t>((n + 255) / 256, 2048);
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); add_k<<<blocks, 256, 0, st>>>(n, s, d); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(add_k, dim3(blocks), dim3(256), 0, st, n, s, d); }
   RUTV_LAUNCH_CK();
 }
 
@@ -247,6 +248,7 @@ struct NcclComm : Comm {
 // k = (j - first_r)/P) <-> piece r, local row k*b + i.
 __global__ void gather_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p, int P, const double* __restrict__ pieces,
                               int64_t piece_rows, double* __restrict__ full, int64_t ldf) {
+  pdl_begin();
   const int64_t tot = nrows * cols;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t gr = e % nrows, c = e / nrows;
@@ -259,6 +261,7 @@ __global__ void gather_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p,
 }
 __global__ void scatter_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p, int P, int r,
                                const double* __restrict__ full, int64_t ldf, double* __restrict__ loc, int64_t ldl) {
+  pdl_begin();
   // local rows of rank r: its blocks j >= p in order
   const int64_t first = p + ((r - p) % P + P) % P;
   const int64_t tot = nrows * cols;  // nrows = global trailing rows; only rank-r rows are written
@@ -273,6 +276,7 @@ __global__ void scatter_rows_k(int64_t nrows, int64_t cols, int64_t b, int64_t p
 // X_loc = the rank-r columns of the rows x rows identity (block-cyclic, width b)
 __global__ void cyclic_identity_k(int64_t rows, int64_t nl, int64_t b, int r, int P, double* __restrict__ X,
                                   int64_t ldx) {
+  pdl_begin();
   const int64_t tot = rows * nl;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e % rows, jl = e / rows;
@@ -533,7 +537,7 @@ class DistFactor {
     for (auto& lr : L) {
       ProfScope _p(st, K_MISC, 0.0);
       count_launch(K_MISC);
-      gather_rows_k<<<grid_for_n(ni * wd), 256, 0, st>>>(ni, wd, b, p, P, lr.w.gath, maxpiece, lr.w.Yfull, ni);
+      launch_k(gather_rows_k, dim3(grid_for_n(ni * wd)), dim3(256), 0, st, ni, wd, b, p, P, lr.w.gath, maxpiece, lr.w.Yfull, ni);
       RUTV_LAUNCH_CK();
     }
   }
@@ -557,7 +561,7 @@ class DistFactor {
       dg(lr.w, st, false, false, ni, b, wd, 1.0, lr.w.q1, ni, lr.w.Uso, wd, 0.0, lr.w.Yfull, ni);
       ProfScope _p(st, K_MISC, 0.0);
       count_launch(K_MISC);
-      scatter_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, p, P, lr.r, lr.w.Yfull, ni, lr.w.Y,
+      launch_k(scatter_rows_k, dim3(grid_for_n(ni * b)), dim3(256), 0, st, ni, b, b, p, P, lr.r, lr.w.Yfull, ni, lr.w.Y,
                                                           std::max<int64_t>(nt[l], 1));
       RUTV_LAUNCH_CK();
     }
@@ -591,7 +595,7 @@ class DistFactor {
       {
         ProfScope _p(st, K_MISC, 0.0);
         count_launch(K_MISC);
-        scatter_rows_k<<<grid_for_n(ni * wd), 256, 0, st>>>(ni, wd, b, p, P, lr.r, out, ni, lr.w.*dst,
+        launch_k(scatter_rows_k, dim3(grid_for_n(ni * wd)), dim3(256), 0, st, ni, wd, b, p, P, lr.r, out, ni, lr.w.*dst,
                                                              std::max<int64_t>(nt[l], 1));
         RUTV_LAUNCH_CK();
       }
@@ -1198,7 +1202,7 @@ int DistFactor::run(randutv_info* info, bool optimistic) {
         if (nc > 0) {
           ProfScope _p(st, K_MISC, 0.0);
           count_launch(K_MISC);
-          scatter_rows_k<<<grid_for_n(nif * mif), 256, 0, st>>>(nif, mif, b, pf, P, lr.r, lr.w.Yfull, nif, lr.w.Y, nc);
+          launch_k(scatter_rows_k, dim3(grid_for_n(nif * mif)), dim3(256), 0, st, nif, mif, b, pf, P, lr.r, lr.w.Yfull, nif, lr.w.Y, nc);
           RUTV_LAUNCH_CK();
           dg(lr.w, st, false, false, r0f, mif, nc, 1.0, lr.T + cs * lr.ldt, lr.ldt, lr.w.Y, nc, 0.0, lr.w.P, r0f);
         } else {
@@ -1268,13 +1272,13 @@ void DistFactor::form_uv(int64_t steps, bool final_block, bool final_fat, int64_
     if (mloc > 0) {
       ProfScope _p(st, K_MISC, 0.0);
       count_launch(K_MISC);
-      cyclic_identity_k<<<grid_for_n(m * mloc), 256, 0, st>>>(m, mloc, b, lr.r, P, lr.U, lr.ldu);
+      launch_k(cyclic_identity_k, dim3(grid_for_n(m * mloc)), dim3(256), 0, st, m, mloc, b, lr.r, P, lr.U, lr.ldu);
       RUTV_LAUNCH_CK();
     }
     if (lr.nl > 0) {
       ProfScope _p(st, K_MISC, 0.0);
       count_launch(K_MISC);
-      cyclic_identity_k<<<grid_for_n(n * lr.nl), 256, 0, st>>>(n, lr.nl, b, lr.r, P, lr.V, lr.ldv);
+      launch_k(cyclic_identity_k, dim3(grid_for_n(n * lr.nl)), dim3(256), 0, st, n, lr.nl, b, lr.r, P, lr.V, lr.ldv);
       RUTV_LAUNCH_CK();
     }
   }
@@ -1308,7 +1312,7 @@ void DistFactor::form_uv(int64_t steps, bool final_block, bool final_fat, int64_
       {
         ProfScope _p(st, K_MISC, 0.0);
         count_launch(K_MISC);
-        gather_rows_k<<<grid_for_n(ni * b), 256, 0, st>>>(ni, b, b, si, P, lr.w.gath, mp, lr.w.Yfull, ni);
+        launch_k(gather_rows_k, dim3(grid_for_n(ni * b)), dim3(256), 0, st, ni, b, b, si, P, lr.w.gath, mp, lr.w.Yfull, ni);
         RUTV_LAUNCH_CK();
       }
       apply_left(lr, lr.V, lr.ldv, lr.nl, si, ni, b, lr.w.Yfull, ni, lr.w.Tv_all + size_t(si) * b * b, b);

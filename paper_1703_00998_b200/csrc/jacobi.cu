@@ -53,6 +53,7 @@ __device__ __forceinline__ JSlot jslot_of(double* work, int k, int mat) {
 
 __global__ void jacobi_init_k(int k, const double* __restrict__ R, int64_t ldr, int64_t strideR,
                               double* __restrict__ work) {
+  pdl_begin();
   const int mat = blockIdx.y;
   const double* Ri = R + int64_t(mat) * strideR;
   const JSlot js = jslot_of(work, k, mat);
@@ -212,6 +213,7 @@ __device__ void store_pair(const double* sB, const double* sW, double* B, double
 // (one launch per round; used when a matrix's blocks do not fit one cluster).
 __global__ void __launch_bounds__(JNT)
 jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ work, double tol) {
+  pdl_begin();
   extern __shared__ __align__(16) double js[];
   __shared__ double nrm[64];
   const int mat = blockIdx.y;
@@ -238,6 +240,7 @@ jacobi_round_k(JacobiDesc d, int sweep, int round, double* __restrict__ work, do
 // cluster-wide rotation count deciding convergence.
 __global__ void __launch_bounds__(JNT)
 jacobi_cluster_k(JacobiDesc d, double* __restrict__ work, double tol) {
+  pdl_begin();
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double js[];
   __shared__ double nrm[64];
@@ -377,6 +380,7 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
 template <int EPL>
 __global__ void __launch_bounds__(JNT)
 jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_sweeps) {
+  pdl_begin();
   constexpr int KB = 16, KP = 32 * EPL;  // block width, padded column length
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double js[];
@@ -527,6 +531,7 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
 __global__ void __launch_bounds__(JNT)
 jacobi_finalize_k(int k, double* __restrict__ work, double* __restrict__ D, double* __restrict__ Us,
                   double* __restrict__ Vs, int* __restrict__ sweeps_out) {
+  pdl_begin();
   extern __shared__ __align__(16) double fs[];
   double* sig = fs;                           // k
   int* rank = reinterpret_cast<int*>(fs + k);  // k
@@ -670,13 +675,15 @@ void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) 
   cfg.blockDim = dim3(JNT, 1, 1);
   cfg.dynamicSmemBytes = smem2;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = csize;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   ProfScope _p(st, K_SVD, 0.0);
   count_launch(K_SVD);
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, work, tol, max_sweeps));
@@ -686,7 +693,7 @@ void launch_init(cudaStream_t st, int batch, int k, const double* R, int64_t ldr
   dim3 g((unsigned)std::min<int64_t>(cdiv(int64_t(k) * k, 256), 64), batch);
   ProfScope _p(st, K_SVD, 0.0);
   count_launch(K_SVD);
-  jacobi_init_k<<<g, 256, 0, st>>>(k, R, ldr, strideR, work);
+  launch_k(jacobi_init_k, dim3(g), dim3(256), 0, st, k, R, ldr, strideR, work);
   RUTV_LAUNCH_CK();
 }
 
@@ -695,7 +702,7 @@ void launch_finalize(cudaStream_t st, int batch, int k, double* work, double* D,
   const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int)) + 16;
   static SmemAttrPerDevice attr_f;
   if (fsmem > 48 * 1024) attr_f.ensure(jacobi_finalize_k, fsmem);
-  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_finalize_k<<<batch, JNT, fsmem, st>>>(k, work, D, Us, Vs, sweeps_out); }
+  { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); launch_k(jacobi_finalize_k, dim3(batch), dim3(JNT), fsmem, st, k, work, D, Us, Vs, sweeps_out); }
   RUTV_LAUNCH_CK();
 }
 }  // namespace
@@ -737,13 +744,15 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
     cfg.blockDim = dim3(32 * d.kb, 1, 1);  // one warp per column pair of a block pair
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = csize;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     ProfScope _p(st, K_SVD, 0.0);
     count_launch(K_SVD);
     RUTV_CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_k, d, work, tol));
@@ -760,7 +769,7 @@ void jacobi_svd_batched(cudaStream_t st, int batch, int k, const double* R, int6
       for (; sweep < end; ++sweep) {
         for (int round = 0; round < d.nb - 1; ++round) {
           dim3 g(d.nb / 2, batch);
-          { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); jacobi_round_k<<<g, JNT, smem, st>>>(d, sweep, round, work, tol); }
+          { ProfScope _p(st, K_SVD, 0.0); count_launch(K_SVD); launch_k(jacobi_round_k, dim3(g), dim3(JNT), smem, st, d, sweep, round, work, tol); }
           RUTV_LAUNCH_CK();
         }
       }

@@ -18,6 +18,7 @@ inline int grid_for(int64_t total) {
 }
 
 __global__ void scale_k(int64_t m, int64_t n, double beta, double* C, int64_t ldc) {
+  pdl_begin();
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
       C[i + j * ldc] = beta == 0.0 ? 0.0 : beta * C[i + j * ldc];
@@ -25,6 +26,7 @@ __global__ void scale_k(int64_t m, int64_t n, double beta, double* C, int64_t ld
 
 __global__ void copy_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds, double* __restrict__ D,
                        int64_t ldd) {
+  pdl_begin();
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
       D[i + j * ldd] = S[i + j * lds];
@@ -33,6 +35,7 @@ __global__ void copy_k(int64_t m, int64_t n, const double* __restrict__ S, int64
 // D (n x m) = S^T (S m x n); 32x32 smem tiles, coalesced both ways
 __global__ void transpose_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds, double* __restrict__ D,
                             int64_t ldd) {
+  pdl_begin();
   __shared__ double t[32][33];
   const int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -47,6 +50,7 @@ __global__ void transpose_k(int64_t m, int64_t n, const double* __restrict__ S, 
 }
 
 __global__ void ident_k(int64_t m, int64_t n, double* D, int64_t ldd, double diagv) {
+  pdl_begin();
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
       D[i + j * ldd] = (i == j) ? diagv : 0.0;
@@ -55,6 +59,7 @@ __global__ void ident_k(int64_t m, int64_t n, double* D, int64_t ldd, double dia
 // Per-block partial sums of squares (fixed partition -> deterministic).
 __global__ void norm_partial_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds,
                                double* __restrict__ D, int64_t ldd, double* partials, int* flag) {
+  pdl_begin();
   __shared__ double red[TB / 32];
   double acc = 0.0;
   int bad = 0;
@@ -80,6 +85,7 @@ __global__ void norm_partial_k(int64_t m, int64_t n, const double* __restrict__ 
 // fixed-order (deterministic) sum of the partials: strided per thread, then a
 // shared-memory tree (one 256-thread block)
 __global__ void norm_final_k(int nparts, const double* partials, double* out2) {
+  pdl_begin();
   __shared__ double red[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += 256) s += partials[i];
@@ -94,6 +100,7 @@ __global__ void norm_final_k(int nparts, const double* partials, double* out2) {
 
 __global__ void gaussian_k(double* G, int64_t ldg, int64_t rows, int64_t cols, uint32_t k0, uint32_t k1,
                            uint32_t step, uint32_t purpose) {
+  pdl_begin();
   const int64_t npairs = (rows + 1) / 2;
   const int64_t total = npairs * cols;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
@@ -107,6 +114,7 @@ __global__ void gaussian_k(double* G, int64_t ldg, int64_t rows, int64_t cols, u
 }
 
 __global__ void diag_block_k(int64_t m, int64_t k, const double* d, double* D, int64_t ldd) {
+  pdl_begin();
   for (int64_t j = blockIdx.y; j < k; j += gridDim.y)
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
       D[i + j * ldd] = (i == j) ? d[j] : 0.0;
@@ -121,41 +129,41 @@ dim3 grid2(int64_t m, int64_t n) {
 
 void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double beta, double* C, int64_t ldc) {
   if (m <= 0 || n <= 0) return;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); scale_k<<<grid2(m, n), TB, 0, st>>>(m, n, beta, C, ldc); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(scale_k, dim3(grid2(m, n)), dim3(TB), 0, st, m, n, beta, C, ldc); }
   RUTV_LAUNCH_CK();
 }
 
 void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0 || S == D) return;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); copy_k<<<grid2(m, n), TB, 0, st>>>(m, n, S, lds, D, ldd); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(copy_k, dim3(grid2(m, n)), dim3(TB), 0, st, m, n, S, lds, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 
 void transpose_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
   dim3 g((unsigned)cdiv(m, 32), (unsigned)cdiv(n, 32));
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); transpose_k<<<g, dim3(32, 8), 0, st>>>(m, n, S, lds, D, ldd); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(transpose_k, dim3(g), dim3(dim3(32, 8)), 0, st, m, n, S, lds, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 
 void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 1.0); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(ident_k, dim3(grid2(m, n)), dim3(TB), 0, st, m, n, D, ldd, 1.0); }
   RUTV_LAUNCH_CK();
 }
 
 void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); ident_k<<<grid2(m, n), TB, 0, st>>>(m, n, D, ldd, 0.0); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(ident_k, dim3(grid2(m, n)), dim3(TB), 0, st, m, n, D, ldd, 0.0); }
   RUTV_LAUNCH_CK();
 }
 
 void copy_norm_check(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D,
                      int64_t ldd, double* scratch, double* out2, int* flag) {
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n, 4096));
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(norm_partial_k, dim3(blocks), dim3(TB), 0, st, m, n, S, lds, (D == S) ? nullptr : D, ldd, scratch, flag); }
   RUTV_LAUNCH_CK();
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 256, 0, st>>>(blocks, scratch, out2); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(norm_final_k, dim3(1), dim3(256), 0, st, blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 
@@ -165,9 +173,9 @@ void fro2(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, d
     return;
   }
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n, 4096));
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_partial_k<<<blocks, TB, 0, st>>>(m, n, S, lds, nullptr, 0, scratch, nullptr); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(norm_partial_k, dim3(blocks), dim3(TB), 0, st, m, n, S, lds, nullptr, 0, scratch, nullptr); }
   RUTV_LAUNCH_CK();
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); norm_final_k<<<1, 256, 0, st>>>(blocks, scratch, out2); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(norm_final_k, dim3(1), dim3(256), 0, st, blocks, scratch, out2); }
   RUTV_LAUNCH_CK();
 }
 
@@ -175,14 +183,14 @@ void gaussian_fill(cudaStream_t st, double* G, int64_t ldg, int64_t rows, int64_
                    uint32_t step, uint32_t purpose) {
   if (rows <= 0 || cols <= 0) return;
   int64_t total = ((rows + 1) / 2) * cols;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); gaussian_k<<<grid_for(total), TB, 0, st>>>(G, ldg, rows, cols, uint32_t(seed & 0xffffffffu),
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(gaussian_k, dim3(grid_for(total)), dim3(TB), 0, st, G, ldg, rows, cols, uint32_t(seed & 0xffffffffu),
                                              uint32_t(seed >> 32), step, purpose); }
   RUTV_LAUNCH_CK();
 }
 
 void write_diag_block(cudaStream_t st, int64_t m, int64_t k, const double* d, double* D, int64_t ldd) {
   if (m <= 0 || k <= 0) return;
-  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); diag_block_k<<<grid2(m, k), TB, 0, st>>>(m, k, d, D, ldd); }
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(diag_block_k, dim3(grid2(m, k)), dim3(TB), 0, st, m, k, d, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 

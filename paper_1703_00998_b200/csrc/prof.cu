@@ -2,6 +2,7 @@
 // bench.py uses it to report gpu_launches and the dominant kernel's achieved
 // throughput (roofline); it is off unless randutv_profile_begin() was called.
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -55,6 +56,16 @@ void launches_by_class(long long* out) {
 }
 
 bool prof_active() { return g_on; }
+
+bool pdl_on() {
+  static const bool on = getenv("RANDUTV_NO_PDL") == nullptr;
+  return on;
+}
+
+long long pdl_max_ctas() {  // one wave of the current device (RANDUTV_PDL_MAX_CTAS: experiments)
+  static const long long env = getenv("RANDUTV_PDL_MAX_CTAS") ? atoll(getenv("RANDUTV_PDL_MAX_CTAS")) : -1;
+  return env >= 0 ? env : (long long)num_sms();
+}
 
 long long launches_total() {
   long long s = 0;

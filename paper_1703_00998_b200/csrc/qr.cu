@@ -103,6 +103,7 @@ template <int W, int RPT>
 __global__ void __launch_bounds__(QR_NT, 1)
 leaf_qr_kernel(int64_t m, int64_t j0, int wj, double* __restrict__ V, int64_t ldv, double* __restrict__ R,
                int64_t ldr, double* __restrict__ tau, double* __restrict__ Tw, int64_t ldt) {
+  pdl_begin();
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ LeafSmem sm;
   extern __shared__ __align__(16) double vsm[];  // [QR_NT*RPT rows][vstride]
@@ -340,13 +341,15 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
   cfg.blockDim = dim3(QR_NT, 1, 1);
   cfg.dynamicSmemBytes = leaf_smem_bytes<W, RPT>();
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   ProfScope _p(st, K_QR, 0.0);
   count_launch(K_QR);
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, m, j0, wj, V, ldv, R, ldr, tau, Tw, ldt));
@@ -358,6 +361,7 @@ void launch_leaf(cudaStream_t st, int C, int64_t m, int64_t j0, int wj, double* 
 __global__ void __launch_bounds__(256)
 qr_small_k(int wj, int64_t b, int splits, const double* __restrict__ part, const double* __restrict__ Tl,
            int64_t ldt, double* __restrict__ O) {
+  pdl_begin();
   __shared__ double sS[32][5];
   __shared__ double sT[32][33];
   __shared__ double red[8][4 * 32 + 1];
@@ -404,6 +408,7 @@ qr_small_k(int wj, int64_t b, int splits, const double* __restrict__ part, const
 
 // zero the strictly-lower part of the b x b R and the whole Tw before a panel
 __global__ void zero_lower_k(int64_t b, double* R, int64_t ldr) {
+  pdl_begin();
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < b * b; idx += int64_t(gridDim.x) * blockDim.x) {
     int64_t r = idx % b, c = idx / b;
     if (r > c) R[r + c * ldr] = 0.0;
@@ -413,6 +418,7 @@ __global__ void zero_lower_k(int64_t b, double* R, int64_t ldr) {
 
 namespace {
 __global__ void reortho_flag_k(const double* stats, double kappa_max, int* flag) {
+  pdl_begin();
   if (threadIdx.x == 0) *flag = !(stats[0] == 0.0 && stats[2] <= kappa_max * stats[1]);
 }
 }  // namespace
@@ -420,7 +426,7 @@ __global__ void reortho_flag_k(const double* stats, double kappa_max, int* flag)
 void reortho_flag(cudaStream_t st, const double* stats, double kappa_max, int* flag) {
   ProfScope _p(st, K_MISC, 0.0);
   count_launch(K_MISC);
-  reortho_flag_k<<<1, 32, 0, st>>>(stats, kappa_max, flag);
+  launch_k(reortho_flag_k, dim3(1), dim3(32), 0, st, stats, kappa_max, flag);
   RUTV_LAUNCH_CK();
 }
 
@@ -446,7 +452,7 @@ int panel_qr_hh(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, d
   const int C = (int)std::max<int64_t>(1, std::min<int64_t>(QR_MAX_CLUSTER, cdiv(m, int64_t(QR_NT) * RPT)));
   set_zero(st, b, b, Tw, ldt);
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); }
-  zero_lower_k<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b * b, 256), 1024)), 256, 0, st>>>(b, R, ldr);
+  launch_k(zero_lower_k, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(b * b, 256), 1024))), dim3(256), 0, st, b, R, ldr);
   RUTV_LAUNCH_CK();
   for (int64_t j0 = 0; j0 < b; j0 += W) {
     const int wj = (int)std::min<int64_t>(W, b - j0);
@@ -467,7 +473,7 @@ int panel_qr_hh(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, d
     {
       ProfScope _p(st, C_QR_SMALL, 0.0);
       count_launch(C_QR_SMALL);
-      qr_small_k<<<(unsigned)cdiv(b, 4), 256, 0, st>>>(wj, b, splits, w.part, Tl, ldt, w.sfull);
+      launch_k(qr_small_k, dim3((unsigned)cdiv(b, 4)), dim3(256), 0, st, wj, b, splits, w.part, Tl, ldt, w.sfull);
       RUTV_LAUNCH_CK();
     }
     if (rest > 0)  // V[j0:, j0+wj:b] -= V_l O(:, j0+wj:b)

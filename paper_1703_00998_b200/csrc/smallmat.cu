@@ -717,6 +717,7 @@ __device__ void init_gram_and_zero(cg::cluster_group& cl, const SmallDims& d, do
 __global__ void __launch_bounds__(SNT, 1)
 chol_inv_k(SmallDims d, double* __restrict__ W, double* __restrict__ R, double* __restrict__ Ri,
            double* __restrict__ stats) {
+  pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
@@ -807,6 +808,7 @@ __device__ __forceinline__ void acc_sub_smem(const double (&acc)[2][2], double* 
 __global__ void __launch_bounds__(SNT, 1)
 chol_inv_dsm_k(SmallDims d, const double* __restrict__ W, double* __restrict__ R, double* __restrict__ Ri,
                double* __restrict__ stats) {
+  pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
@@ -965,6 +967,7 @@ struct LuSm {
 __global__ void __launch_bounds__(SNT, 1)
 lu_dsm_k(SmallDims dd, double* __restrict__ F, double* __restrict__ Li, double* __restrict__ Ui,
          double* __restrict__ S, double* __restrict__ US) {
+  pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   LuSm& q = *reinterpret_cast<LuSm*>(sm_raw);
@@ -1147,6 +1150,7 @@ struct ReconArgs {
 // Also zero-pads F (written by the b x b GEMM F = -Q(0:b,:) R2^-1 next) and
 // zeroes the strictly-lower tiles of R2, R2^-1.
 __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
+  pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
@@ -1240,6 +1244,7 @@ __global__ void __launch_bounds__(SNT, 1) recon_r2_k(ReconArgs a) {
 // L^-1, U~^-1 built along; then US = U~ S.  Zeroes the tiles of Li above and
 // of Ui / US below the diagonal first.
 __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
+  pdl_begin();
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double sm_raw[];
   SmallSm& s = *reinterpret_cast<SmallSm*>(sm_raw);
@@ -1277,6 +1282,7 @@ __global__ void __launch_bounds__(SNT, 1) recon_lu_k(ReconArgs a) {
 __global__ void recon_finish_k(int b, int bp, const double* __restrict__ S, const double* __restrict__ RR,
                                double* __restrict__ Rh, int64_t ldr, double* __restrict__ Tw, int64_t ldt,
                                double* __restrict__ tau) {
+  pdl_begin();
   for (int c = blockIdx.x; c < b; c += gridDim.x)
     for (int r = threadIdx.x; r < b; r += blockDim.x) {
     Rh[r + c * ldr] = (r <= c) ? S[r] * RR[r + int64_t(c) * bp] : 0.0;
@@ -1287,6 +1293,7 @@ __global__ void recon_finish_k(int b, int bp, const double* __restrict__ S, cons
 
 // V(0:b, 0:b) <- unit lower L (strict lower part of F, ld bp)
 __global__ void put_unit_lower_k(int b, const double* __restrict__ F, int bp, double* __restrict__ V, int64_t ldv) {
+  pdl_begin();
   for (int c = blockIdx.x; c < b; c += gridDim.x)
     for (int r = threadIdx.x; r < b; r += blockDim.x) {
     V[r + c * ldv] = (r > c) ? F[r + int64_t(c) * bp] : (r == c ? 1.0 : 0.0);
@@ -1304,13 +1311,15 @@ void launch_cluster_smem(K kern, cudaStream_t st, int C, size_t smem, Args... ar
   cfg.blockDim = dim3(SNT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
@@ -1333,13 +1342,15 @@ void launch_cluster(K kern, cudaStream_t st, int C, Args... args) {
   cfg.blockDim = dim3(SNT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   RUTV_CK(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 }  // namespace
@@ -1443,7 +1454,7 @@ void small_recon(cudaStream_t st, int64_t b, const SmallWork& w, const double* Q
   {
     ProfScope _p(ts, C_QR_SMALL, 0.0);
     count_launch(C_QR_SMALL);
-    recon_finish_k<<<(int)std::min<int64_t>(b, 256), 256, 0, ts>>>((int)b, bp, w.S, w.W2, R, ldr, Tw,
+    launch_k(recon_finish_k, dim3((int)std::min<int64_t>(b, 256)), dim3(256), 0, ts, (int)b, bp, w.S, w.W2, R, ldr, Tw,
                                                                                     ldt, tau);
     RUTV_LAUNCH_CK();
   }
@@ -1454,7 +1465,7 @@ void small_put_unit_lower(cudaStream_t st, int64_t b, const SmallWork& w, double
   ProfScope _p(st, K_MISC, 0.0);
   count_launch(K_MISC);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(b * b, 256), 512));
-  put_unit_lower_k<<<blocks, 256, 0, st>>>((int)b, w.F, w.bp, V, ldv);
+  launch_k(put_unit_lower_k, dim3(blocks), dim3(256), 0, st, (int)b, w.F, w.bp, V, ldv);
   RUTV_LAUNCH_CK();
 }
 
