@@ -45,6 +45,9 @@ GEMM_CASES = [
     (1, 1, 1, False, False), (37, 29, 41, False, False), (130, 257, 33, True, False), (255, 129, 300, False, True),
     (128, 128, 16, True, True), (2000, 256, 3000, True, False), (32, 256, 10000, True, False),
     (3001, 513, 256, False, True), (64, 64, 0, False, False),
+    # even leading dimensions, ragged M / N / K: the TMA-staged tiles (zero-filled edges)
+    (1002, 250, 998, False, False), (1002, 250, 998, True, False), (1002, 250, 998, False, True),
+    (1002, 250, 998, True, True), (2050, 1090, 300, False, True),
 ]
 
 
@@ -62,6 +65,18 @@ def test_dgemm_vs_oracle_matmul(M, N, K, ta, tb, beta):
     got = to_host(C)
     bound = (K + 2) * EPS * (np.abs(A.T if ta else A) @ np.abs(B.T if tb else B) * abs(alpha) + abs(beta) * np.abs(C0))
     assert np.all(np.abs(got - ref) <= 2 * bound + 1e-300)
+
+
+def test_dgemm_tma_path():
+    """The TMA-staged tile variant (RANDUTV_GEMM_TMA=1, profiles/r02_tma_ab.md) on the same
+    parity cases, in a fresh process (the switch is read once per process)."""
+    import subprocess
+    import sys
+    import os
+    env = dict(os.environ, RANDUTV_GEMM_TMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "test_dgemm_vs_oracle_matmul"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_dgemm_misaligned_views():
