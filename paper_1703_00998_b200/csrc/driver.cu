@@ -113,6 +113,7 @@ Plan make_plan(int64_t m, int64_t n, int64_t b, int q, bool uv, int64_t ovs = 0)
 struct Work {
   double *G, *Y, *Y2, *P, *P2, *Vu, *Wt, *Wt2, *tau, *Rtmp, *Ttmp;
   double *WG, *H;  // look-ahead sketch: [W_u | G'] (m x (b + bs)), H = W_u^T G' (b x bs)
+  double* Zp;            // X Y before the deferred R^-1 of the power loop (m x bs, R26)
   double *Pbig, *part2;  // P_big = T(:, J3) Q1(b:, :) (m x b) and its split-K scratch (side stream)
   double *LT, *MT;       // L T_v, M T_v (b x b): the P2 assembly's right factors (read on two streams)
   size_t part2_elems;
@@ -150,6 +151,7 @@ Work carve(Arena& ar, const Plan& p) {
     w.Vso = ar.take<double>(size_t(bs) * bs);
     w.jworko = ar.take<double>(jacobi_work_elems(1, (int)bs));
   }
+  w.Zp = ar.take<double>(size_t(m) * bs);
   w.P = ar.take<double>(size_t(m) * b);
   w.P2 = ar.take<double>(size_t(m) * b);
   w.Pbig = ar.take<double>(size_t(m) * b);
@@ -280,7 +282,7 @@ cudaStream_t crit_stream() {
 }
 
 cudaEvent_t overlap_event(int which) {
-  static cudaEvent_t evs[12][64] = {};
+  static cudaEvent_t evs[16][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (!evs[which][dev]) RUTV_CK(cudaEventCreateWithFlags(&evs[which][dev], cudaEventDisableTiming));
@@ -427,6 +429,15 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
                         jacobi_single_launch((int)(b + o.oversample)) && !getenv("RANDUTV_NO_GRAPH") &&
                         !getenv("RANDUTV_POISON_WORKSPACE");
   const bool defer_y = graph_ok;
+  static const bool defer_reortho_env = [] {  // RANDUTV_NO_DEFER_REORTHO=1: A/B switch
+    const char* e = getenv("RANDUTV_NO_DEFER_REORTHO");
+    return !(e && atoi(e) != 0);
+  }();
+  const bool defer_reortho = defer_reortho_env && opt_y;
+  static const bool sweep_at_defer = [] {  // RANDUTV_SWEEP_AT_DEFER=0/1: A/B switch
+    const char* e = getenv("RANDUTV_SWEEP_AT_DEFER");
+    return e ? atoi(e) != 0 : true;
+  }();
 
   auto enqueue_all = [&]() {
   bool final_tall = false, final_fat = false;
@@ -581,7 +592,28 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
           if (reortho) {
             // not beside the first chain of a look-ahead step: the left update
             // GEMM of the previous step fills the SMs there
-            if (!(use_y0 && it == 0)) svd_sweep_here();
+            if (!(use_y0 && it == 0) && !(defer_reortho && !sweep_at_defer)) svd_sweep_here();
+            // R26: Z = X (Y R^-1) = (X Y) R^-1 -- the Gram and the Cholesky run
+            // on the priority stream while X Y runs here; only the TRMM stays
+            // on the critical path.  The kappa decision is a device flag like
+            // the others (a failure redoes the step's sketch synchronously).
+            QrWork qd = qwy;
+            qd.part = w.part2;  // the priority stream's own split-K scratch
+            qd.part_elems = w.part2_elems;
+            cudaEvent_t f = overlap_event(12), j = overlap_event(13);
+            if (defer_reortho) {
+              RUTV_CK(cudaEventRecord(f, st));
+              RUTV_CK(cudaStreamWaitEvent(priority_stream(), f, 0));
+            }
+            if (defer_reortho && reortho_defer_begin(priority_stream(), ni, bw, Ycur, n, qd)) {
+              RUTV_CK(cudaEventRecord(j, priority_stream()));
+              ensure_lu();
+              dg(w, st, false, false, mi, bw, ni, 1.0, X, m, Ycur, n, 0.0, w.Zp, m);     // Zp = X Y
+              RUTV_CK(cudaStreamWaitEvent(st, j, 0));
+              reortho_defer_apply(st, mi, bw, w.Zp, m, w.G, m, qwy);                   // Z = Zp R^-1
+              dg(w, st, true, false, ni, bw, mi, 1.0, X, m, w.G, m, 0.0, Ycur, n);      // Y = X^T Z
+              continue;
+            }
             check_qr(rutv::reortho(st, ni, bw, Ycur, n, Yalt, n, w.Rtmp, w.Ttmp, w.tau, qwy));
             std::swap(Ycur, Yalt);
           }

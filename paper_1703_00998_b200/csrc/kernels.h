@@ -143,6 +143,17 @@ size_t qr_work_elems(int64_t b);
 // be overwritten.
 int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, double* Q, int64_t ldq, double* tmp_bb,
             double* Tmp_bb, double* tau, const QrWork& w);
+// The same CholeskyQR re-orthonormalisation with its triangular factor
+// applied AFTER the next product of the power loop (R26):
+//   Z = X (Y R^-1) = (X Y) R^-1,
+// so that X Y runs concurrently with the Gram and the Cholesky (optimistic
+// mode only: begin returns false -- nothing enqueued -- otherwise).
+// begin (stream hs): G = Y^T Y, R, R^-1 and the kappa decision flag in the
+// next dev_flags slot; apply (stream st, after begin's work): Z = Zp R^-1
+// (rows x b TRMM).  w.part must be scratch no concurrent GEMM uses.
+bool reortho_defer_begin(cudaStream_t hs, int64_t m, int64_t b, const double* Y, int64_t ldy, const QrWork& w);
+void reortho_defer_apply(cudaStream_t st, int64_t rows, int64_t b, const double* Zp, int64_t ldzp, double* Z,
+                         int64_t ldz, const QrWork& w);
 // Householder QR of the m x b panel held in V (ld ldv), in place:
 // on exit V is the explicit unit-lower-trapezoidal reflector matrix, R (b x b,
 // ld ldr) the upper-triangular factor (zeros below), tau[b] the reflector

@@ -556,6 +556,10 @@ void read_stats_sync(cudaStream_t st, const double* dstats, double (&h)[3]) {
   RUTV_CK(cudaStreamSynchronize(st));
 }
 
+// kappa(R1) estimated by its diagonal: CholeskyQR's loss of orthogonality
+// ~ kappa^2 eps stays <= 1e-8 -- ample for a basis of the power loop
+constexpr double kReorthoKappaMax = 1e4;
+
 bool cholqr_ok(const QrWork& w, int64_t m, int64_t b) {
   return w.mode == 0 && w.q1 && w.small && size_t(m) * b <= w.q1_elems && b <= 512;
 }
@@ -660,9 +664,7 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
     const int bp = sw.bp;
     dgemm(st, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);
     small_chol_inv(st, b, sw);
-    // kappa(R1) estimated by its diagonal: CholeskyQR's loss of orthogonality
-    // ~ kappa^2 eps stays <= 1e-8 -- ample for a basis of the power loop
-    constexpr double kKappaMax = 1e4;
+    constexpr double kKappaMax = kReorthoKappaMax;
     bool ok;
     if (w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap) {
       reortho_flag(st, sw.stats, kKappaMax, w.dev_flags + (*w.flag_count)++);
@@ -682,6 +684,23 @@ int reortho(cudaStream_t st, int64_t m, int64_t b, double* Y, int64_t ldy, doubl
   if (rc != OK) return rc;
   thin_q(st, m, b, Y, ldy, Tmp_bb, b, Q, ldq, tmp_bb, w.part, w.part_elems);
   return OK;
+}
+
+bool reortho_defer_begin(cudaStream_t hs, int64_t m, int64_t b, const double* Y, int64_t ldy, const QrWork& w) {
+  if (!cholqr_ok(w, m, b) || !(w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap)) return false;
+  GemmRole role(C_GEMM_QR);
+  SmallWork sw = carve_small(w.small, b);
+  dgemm(hs, true, false, b, b, m, 1.0, Y, ldy, Y, ldy, 0.0, sw.W1, sw.bp, w.part, w.part_elems, 0, false, true);
+  small_chol_inv(hs, b, sw);
+  reortho_flag(hs, sw.stats, kReorthoKappaMax, w.dev_flags + (*w.flag_count)++);
+  return true;
+}
+
+void reortho_defer_apply(cudaStream_t st, int64_t rows, int64_t b, const double* Zp, int64_t ldzp, double* Z,
+                         int64_t ldz, const QrWork& w) {
+  GemmRole role(C_GEMM_QR);
+  SmallWork sw = carve_small(w.small, b);
+  dgemm(st, false, false, rows, b, b, 1.0, Zp, ldzp, sw.R1i, sw.bp, 0.0, Z, ldz, w.part, w.part_elems, 0, true);
 }
 
 void thin_q(cudaStream_t st, int64_t m, int64_t b, const double* V, int64_t ldv, const double* Tw, int64_t ldt,
