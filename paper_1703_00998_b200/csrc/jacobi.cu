@@ -661,6 +661,9 @@ size_t jacobi_work_elems(int batch, int k) { return size_t(batch) * size_t(jslot
 namespace {
 // up to max_sweeps sweeps of jacobi_cluster2_k on every matrix of the batch
 void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) {
+  // RANDUTV_EXP_NO_SWEEPS=1: timing experiment only (skips the sweeps: wrong results)
+  static const bool exp_skip = getenv("RANDUTV_EXP_NO_SWEEPS") && atoi(getenv("RANDUTV_EXP_NO_SWEEPS"));
+  if (exp_skip) return;
   JacobiDesc d = make_desc(k);
   const int csize = d.nb / 2;
   const double tol = double(k) * DBL_EPSILON;
