@@ -29,3 +29,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgem
     -o $O/${TAG}_gemm python tools/prof_gemm.py > $O/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 [ -x tools/chol_bench ] && timeout 600 ncu --set full --clock-control none --import-source on -k regex:chol_inv_dsm \
     -s 1 -c 1 -o $O/${TAG}_chol ./tools/chol_bench 256 1e3 > $O/${TAG}_ncu_chol.log 2>&1; echo "ncu chol rc=$?"
+timeout 600 python tools/gemm_steps.py > $O/${TAG}_gemm_steps.txt 2>&1; echo "gemm steps rc=$?"
+RANDUTV_EXP_NO_SWEEPS=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-utv \
+    > $O/${TAG}_bench_nosweeps.json 2>/dev/null; echo "no-sweeps timing rc=$?"
+cuobjdump -sass paper_1703_00998_b200/_randutv.so > /tmp/sass.txt 2>/dev/null && \
+  for op in DMMA LDGSTS UTMALDG UTMASTG DFMA HMMA UTCHMMA UTCQMMA; do echo "$op $(grep -c "$op" /tmp/sass.txt)"; done \
+  > $O/${TAG}_sass_counts.txt
