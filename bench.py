@@ -195,7 +195,25 @@ def critical_path(tl):
     chain = [(a, e) for a, e, c in main if c in ("qr_small", "gemm_panel_qr")]
     chain_ms = sum(e - a for a, e in chain)
     exposed = sum((e - a) - covered(a, e) for a, e in chain)
+    # stricter: span time in which no big GEMM (sketch / right / left apply) runs on
+    # ANY stream -- the exposed latency-bound chains wherever they run, plus the tail
+    # after the last big GEMM (the last SVD chunk and the folds)
+    big = sorted((a, e) for c, s, a, e in tl if c in ("gemm_sketch", "gemm_right_apply", "gemm_left_apply"))
+    t0 = min(a for _, _, a, _ in tl)
+    t1 = max(e for _, _, _, e in tl)
+    union, cur = 0.0, None
+    for a, e in big:
+        if cur is None or a > cur[1]:
+            if cur is not None:
+                union += cur[1] - cur[0]
+            cur = [a, e]
+        else:
+            cur[1] = max(cur[1], e)
+    if cur is not None:
+        union += cur[1] - cur[0]
+    last_big = max((e for _, e in big), default=t0)
     return {"factorization_span": round(span, 3), "main_busy": round(sum(busy.values()), 3),
+            "no_big_gemm": round((t1 - t0) - union, 3), "tail_after_last_big_gemm": round(t1 - last_big, 3),
             "main_idle": round(span - sum(busy.values()), 3),
             "main_by_class": {k: round(v, 3) for k, v in sorted(busy.items(), key=lambda t: -t[1])},
             "qr_chain_main": round(chain_ms, 3), "qr_chain_main_exposed": round(exposed, 3),
