@@ -331,7 +331,7 @@ __device__ __forceinline__ double rcp_fast(double x) {
 // total of value L & 3); t = 2 gamma sgn(d) / (|d| + sqrt(d^2 + 4 gamma^2)),
 // d = beta - alpha -- the classical t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
 // zeta = d / (2 gamma), with one reciprocal and no overflow for small gamma.
-template <int EPL>
+template <int EPL, bool FAST>
 __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCol<EPL>& xw, JacCol<EPL>& yw,
                                          double tol) {
   const int lane = threadIdx.x & 31;
@@ -358,7 +358,12 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
   const double al = __shfl_sync(0xffffffffu, v[0], 0);
   const double be = __shfl_sync(0xffffffffu, v[0], 1);
   const double ga = __shfl_sync(0xffffffffu, v[0], 2);
-  if (!(ga != 0.0 && fabs(ga) > tol * sqrt(al * be))) return 0;
+  // FAST: the threshold test squared (no IEEE sqrt on the dependent chain)
+  if constexpr (FAST) {
+    if (!(ga != 0.0 && ga * ga > (tol * tol) * (al * be))) return 0;
+  } else {
+    if (!(ga != 0.0 && fabs(ga) > tol * sqrt(al * be))) return 0;
+  }
   const double d = be - al, g2 = 2.0 * ga;
   const double h = fma(d, d, g2 * g2);
   const double root = h * rsqrt(h);
@@ -377,7 +382,7 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
   return 1;
 }
 
-template <int EPL>
+template <int EPL, bool FAST>
 __global__ void __launch_bounds__(JNT)
 jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_sweeps) {
   pdl_begin();
@@ -473,7 +478,7 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
           jc_lds(yb, cbq, lane);
           jc_lds(xw, cwp, lane);
           jc_lds(yw, cwq, lane);
-          if (jc_rotate(xb, yb, xw, yw, tol)) {
+          if (jc_rotate<EPL, FAST>(xb, yb, xw, yw, tol)) {
             jc_sts(cbp, xb, lane);
             jc_sts(cbq, yb, lane);
             jc_sts(cwp, xw, lane);
@@ -497,7 +502,7 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
         JacCol<EPL> yb, yw;
         jc_lds(yb, cbq, lane);
         jc_lds(yw, cwq, lane);
-        if (jc_rotate(xb, yb, xw, yw, tol)) {
+        if (jc_rotate<EPL, FAST>(xb, yb, xw, yw, tol)) {
           jc_sts(cbq, yb, lane);
           jc_sts(cwq, yw, lane);
           ++rot;
@@ -669,9 +674,21 @@ void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) 
   const double tol = double(k) * DBL_EPSILON;
   const int epl = k <= 64 ? 2 : (k <= 128 ? 4 : 8);
   const size_t smem2 = size_t(2) * 2 * 16 * 32 * epl * sizeof(double);
-  auto kern = epl == 2 ? jacobi_cluster2_k<2> : (epl == 4 ? jacobi_cluster2_k<4> : jacobi_cluster2_k<8>);
-  static OncePerDevice attr2[3];
-  const int ai = epl == 2 ? 0 : (epl == 4 ? 1 : 2);
+  // the squared threshold test (bitwise the same rotations, no IEEE sqrt on the
+  // sub-round's dependent chain): k = 256 single matrix 5.85 -> 5.41 ms, c3
+  // 250.4 -> 249.1 ms; for k <= 128 (c2) it measured 0.45 ms slower in the
+  // factorization (ptxas spills the EPL = 4 variant), so k > 128 only.
+  // RANDUTV_JACOBI_FASTROT=0 / 1: A/B switch
+  static const int fast_env = [] {
+    const char* e = getenv("RANDUTV_JACOBI_FASTROT");
+    return e ? atoi(e) : -1;
+  }();
+  const bool fast = fast_env < 0 ? epl == 8 : fast_env != 0;
+  using KernT = void (*)(JacobiDesc, double*, double, int);
+  KernT kern = fast ? (epl == 2 ? jacobi_cluster2_k<2, true> : (epl == 4 ? jacobi_cluster2_k<4, true> : jacobi_cluster2_k<8, true>))
+                    : (epl == 2 ? jacobi_cluster2_k<2, false> : (epl == 4 ? jacobi_cluster2_k<4, false> : jacobi_cluster2_k<8, false>));
+  static OncePerDevice attr2[6];
+  const int ai = (epl == 2 ? 0 : (epl == 4 ? 1 : 2)) + (fast ? 3 : 0);
   attr2[ai]([&] { RUTV_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2)); });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(csize, batch, 1);
