@@ -384,7 +384,7 @@ __device__ __forceinline__ int jc_rotate(JacCol<EPL>& xb, JacCol<EPL>& yb, JacCo
 
 template <int EPL, bool FAST>
 __global__ void __launch_bounds__(JNT)
-jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_sweeps) {
+jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_sweeps, int pair_load) {
   pdl_begin();
   constexpr int KB = 16, KP = 32 * EPL;  // block width, padded column length
   cg::cluster_group cluster = cg::this_cluster();
@@ -425,6 +425,42 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
       sW[(slot * KB + c) * KP + r] = ok ? __ldcg(W + r + int64_t(g) * k) : 0.0;
     }
   };
+  // both blocks of a round at once, every load issued before the first shared
+  // store (one L2 round trip instead of one per loop iteration: ncu showed
+  // long-scoreboard stalls at ~12 % of the issue cycles)
+  auto load_pair = [&](int bp, int bq) {
+    if (!vec) {
+      load_block(bp, 0);
+      load_block(bq, 1);
+      return;
+    }
+    constexpr int IT = (KB * KP / 2 + JNT - 1) / JNT;  // double2 per thread per block
+    double2 vb[2][IT], vw[2][IT];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+      for (int u = 0; u < IT; ++u) {
+        const int idx = threadIdx.x + u * JNT;
+        const int c = idx / (KP / 2), r = 2 * (idx % (KP / 2)), g = (sl ? bq : bp) * KB + c;
+        const bool ok = idx < KB * KP / 2 && g < k && r < k;
+        vb[sl][u] = vw[sl][u] = make_double2(0.0, 0.0);
+        if (ok) {
+          vb[sl][u] = __ldcg(reinterpret_cast<const double2*>(B + r + int64_t(g) * k));
+          vw[sl][u] = __ldcg(reinterpret_cast<const double2*>(W + r + int64_t(g) * k));
+        }
+      }
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+      for (int u = 0; u < IT; ++u) {
+        const int idx = threadIdx.x + u * JNT;
+        if (idx < KB * KP / 2) {
+          const int c = idx / (KP / 2), r = 2 * (idx % (KP / 2));
+          *reinterpret_cast<double2*>(sB + (sl * KB + c) * KP + r) = vb[sl][u];
+          *reinterpret_cast<double2*>(sW + (sl * KB + c) * KP + r) = vw[sl][u];
+        }
+      }
+  };
   auto store_block = [&](int blk, int slot) {
     if (vec) {
       for (int idx = threadIdx.x; idx < KB * KP / 2; idx += JNT) {
@@ -460,8 +496,12 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
     for (int round = 0; round < d.nb - 1; ++round) {
       int bp, bq;
       rr_pair(d.nb, round, cta, bp, bq);
-      load_block(bp, 0);
-      load_block(bq, 1);
+      if (pair_load) {
+        load_pair(bp, bq);
+      } else {
+        load_block(bp, 0);
+        load_block(bq, 1);
+      }
       __syncthreads();
       if (round == 0) {
         // within-block pairs of both blocks: warp w -> block w / 8, pair w % 8
@@ -684,7 +724,11 @@ void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) 
     return e ? atoi(e) : -1;
   }();
   const bool fast = fast_env < 0 ? epl == 8 : fast_env != 0;
-  using KernT = void (*)(JacobiDesc, double*, double, int);
+  using KernT = void (*)(JacobiDesc, double*, double, int, int);
+  static const int pair_load = [] {  // RANDUTV_JACOBI_PAIRLOAD=0: A/B switch
+    const char* e = getenv("RANDUTV_JACOBI_PAIRLOAD");
+    return e ? atoi(e) : 1;
+  }();
   KernT kern = fast ? (epl == 2 ? jacobi_cluster2_k<2, true> : (epl == 4 ? jacobi_cluster2_k<4, true> : jacobi_cluster2_k<8, true>))
                     : (epl == 2 ? jacobi_cluster2_k<2, false> : (epl == 4 ? jacobi_cluster2_k<4, false> : jacobi_cluster2_k<8, false>));
   static OncePerDevice attr2[6];
@@ -706,7 +750,7 @@ void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) 
   cfg.numAttrs = pdl_on() ? 2 : 1;
   ProfScope _p(st, K_SVD, 0.0);
   count_launch(K_SVD);
-  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, work, tol, max_sweeps));
+  RUTV_CK(cudaLaunchKernelEx(&cfg, kern, d, work, tol, max_sweeps, pair_load));
 }
 
 void launch_init(cudaStream_t st, int batch, int k, const double* R, int64_t ldr, int64_t strideR, double* work) {
