@@ -496,7 +496,7 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
     for (int round = 0; round < d.nb - 1; ++round) {
       int bp, bq;
       rr_pair(d.nb, round, cta, bp, bq);
-      if (pair_load) {
+      if (pair_load & 1) {
         load_pair(bp, bq);
       } else {
         load_block(bp, 0);
@@ -554,7 +554,10 @@ jacobi_cluster2_k(JacobiDesc d, double* __restrict__ work, double tol, int max_s
       __syncthreads();
       store_block(bp, 0);
       store_block(bq, 1);
-      __threadfence();
+      // the cluster barrier is a release / acquire at cluster scope: it orders
+      // these global stores before the other CTAs' loads of the next round
+      // (the extra GPU-scope fence cost ~5 % of the issue stalls, ncu)
+      if (!(pair_load & 2)) __threadfence();
       cluster.sync();
     }
     if (lane == 0 && rot) atomicAdd(&rot_sm, rot);
@@ -725,9 +728,10 @@ void launch_c2(cudaStream_t st, int batch, int k, double* work, int max_sweeps) 
   }();
   const bool fast = fast_env < 0 ? epl == 8 : fast_env != 0;
   using KernT = void (*)(JacobiDesc, double*, double, int, int);
-  static const int pair_load = [] {  // RANDUTV_JACOBI_PAIRLOAD=0: A/B switch
+  // bit 0: load_pair, bit 1: no per-round GPU-scope fence (RANDUTV_JACOBI_PAIRLOAD: A/B switch)
+  static const int pair_load = [] {
     const char* e = getenv("RANDUTV_JACOBI_PAIRLOAD");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 3;
   }();
   KernT kern = fast ? (epl == 2 ? jacobi_cluster2_k<2, true> : (epl == 4 ? jacobi_cluster2_k<4, true> : jacobi_cluster2_k<8, true>))
                     : (epl == 2 ? jacobi_cluster2_k<2, false> : (epl == 4 ? jacobi_cluster2_k<4, false> : jacobi_cluster2_k<8, false>));
