@@ -445,7 +445,14 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // the single-cluster Jacobi kernel they run in chunks on the side stream.
   // steps per SVD chunk, measured at c3 with the incremental sweeps:
   // 4 / 6 / 8 / 10 / 12 = 269.0 / 268.0 / 265.3 / 266.6 / 268.0 ms
-  constexpr int64_t kSvdChunk = 8;
+  // Factorizations with few steps (c1: 9, c2: 23) get shorter chunks so that
+  // their SVDs start early and sweep beside the latency-bound chains instead
+  // of all landing in the tail (RANDUTV_SVD_CHUNK=n forces n: A/B switch).
+  static const int env_chunk = [] {
+    const char* e = getenv("RANDUTV_SVD_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t kSvdChunk = env_chunk > 0 ? env_chunk : std::max<int64_t>(2, std::min<int64_t>(8, p.nrand / 4));
   int64_t svd_done = 0;
   struct SvdChunk {
     int64_t s0, s1;
@@ -457,6 +464,10 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // re-orthonormalisations and QR(Y), when most SMs are idle), and are
   // finished when the next chunk starts; otherwise a chunk runs in one go.
   const bool svd_incr = svd_side && jacobi_incremental((int)b);
+  static const bool merge_tail = [] {  // RANDUTV_SVD_MERGE_TAIL=0: A/B switch
+    const char* e = getenv("RANDUTV_SVD_MERGE_TAIL");
+    return e ? atoi(e) != 0 : true;
+  }();
   struct ActiveChunk {
     int64_t s0 = 0, s1 = 0;
     bool on = false;
@@ -486,7 +497,12 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     RUTV_CK(cudaStreamWaitEvent(side, e, 0));
     jacobi_sweeps(side, (int)(active.s1 - active.s0), (int)b, chunk_work(active.s0), 1);  // 1 / 2 / 3 per window: 265.3 / 267.5 / 269.5 ms
   };
-  auto launch_svd_chunk = [&]() {
+  // merge (after the loop): the last steps' SVDs join the still active chunk
+  // -- one launch finishes both (each matrix resumes from its own sweep), so
+  // the tail holds one SVD latency instead of the active chunk's remaining
+  // sweeps followed by a fresh chunk (c1: all 9 SVDs were in the tail, c2 ~14
+  // + the rest of the previous chunk)
+  auto launch_svd_chunk = [&](bool merge) {
     if (steps <= svd_done) return;
     cudaEvent_t e;
     RUTV_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -494,7 +510,10 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     RUTV_CK(cudaEventRecord(e, st));
     RUTV_CK(cudaStreamWaitEvent(side, e, 0));
     const int64_t s0 = svd_done, cnt = steps - svd_done;
-    if (svd_incr) {
+    if (svd_incr && merge && merge_tail && active.on && active.s1 == s0) {
+      jacobi_begin(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
+      active.s1 = steps;
+    } else if (svd_incr) {
       finish_active();
       jacobi_begin(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
       active.s0 = s0;
@@ -813,7 +832,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
           if (on_final) on_final(b * chunks[folded].s1, st);
           ++folded;
         }
-        launch_svd_chunk();
+        launch_svd_chunk(false);
       }
       if (o.tol > 0.0) {
         double t2 = 0.0;
@@ -861,7 +880,7 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   set_gemm_role(C_GEMM_OTHER);
   // ---- batched small SVDs
   if (svd_side) {
-    launch_svd_chunk();
+    launch_svd_chunk(true);
     finish_active();
   } else if (steps > 0) {
     jacobi_svd_batched(st, (int)steps, (int)b, w.Rall, b, b * b, w.Dall, w.Usall, w.Vsall, w.jwork, w.sweeps);
