@@ -230,9 +230,10 @@ void dg(const Work& w, cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, 
 // Low-priority side stream per device for work off the critical path (the
 // deferred b x b SVDs): its kernels fill the SMs the latency-bound panel-QR
 // kernels leave idle, and the block scheduler prefers the main stream's CTAs.
-// which = 0: deferred SVD chunks; 1: trailing right-apply updates; 2: D2H copies of final T blocks.
+// which = 0: deferred SVD chunks; 1: trailing right-apply updates; 2: D2H copies of final T blocks;
+// 3: the last SVD chunk after the loop (concurrent with the end of the previous one).
 cudaStream_t side_stream(int which = 0) {
-  static cudaStream_t streams[3][64] = {};
+  static cudaStream_t streams[4][64] = {};
   int dev = 0;
   RUTV_CK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return nullptr;
@@ -464,9 +465,12 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
   // re-orthonormalisations and QR(Y), when most SMs are idle), and are
   // finished when the next chunk starts; otherwise a chunk runs in one go.
   const bool svd_incr = svd_side && jacobi_incremental((int)b);
-  static const bool merge_tail = [] {  // RANDUTV_SVD_MERGE_TAIL=0: A/B switch
-    const char* e = getenv("RANDUTV_SVD_MERGE_TAIL");
-    return e ? atoi(e) != 0 : true;
+  // after the loop: 0 = finish the active chunk, then the last steps' chunk
+  // (sequential), 1 = one merged launch, 2 = both concurrently on two streams
+  // (RANDUTV_SVD_TAIL: A/B switch)
+  static const int tail_mode = [] {
+    const char* e = getenv("RANDUTV_SVD_TAIL");
+    return e ? atoi(e) : 2;
   }();
   struct ActiveChunk {
     int64_t s0 = 0, s1 = 0;
@@ -510,9 +514,25 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     RUTV_CK(cudaEventRecord(e, st));
     RUTV_CK(cudaStreamWaitEvent(side, e, 0));
     const int64_t s0 = svd_done, cnt = steps - svd_done;
-    if (svd_incr && merge && merge_tail && active.on && active.s1 == s0) {
+    if (svd_incr && merge && tail_mode == 1 && active.on && active.s1 == s0) {
       jacobi_begin(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
       active.s1 = steps;
+    } else if (svd_incr && merge && tail_mode == 2) {
+      // the active chunk's remaining sweeps on the SVD stream, the last steps'
+      // SVDs on a second one, concurrently: the tail holds one SVD latency and
+      // the earlier chunk's folds run behind the last chunk's sweeps
+      finish_active();
+      cudaStream_t side3 = side_stream(3);
+      RUTV_CK(cudaStreamWaitEvent(side3, e, 0));
+      jacobi_begin(side3, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
+      jacobi_end(side3, (int)cnt, (int)b, chunk_work(s0), w.Dall + s0 * b, w.Usall + size_t(s0) * b * b,
+                 w.Vsall + size_t(s0) * b * b, w.sweeps + s0);
+      cudaEvent_t done;
+      RUTV_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      evs.push_back(done);
+      RUTV_CK(cudaEventRecord(done, side3));
+      // the caller's stream joins side3 through the fold chain (main waits on done)
+      chunks.push_back({s0, steps, done});
     } else if (svd_incr) {
       finish_active();
       jacobi_begin(side, (int)cnt, (int)b, w.Rall + size_t(s0) * b * b, b, b * b, chunk_work(s0));
