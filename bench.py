@@ -293,10 +293,6 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if use_dist:
-        # keep NCCL's communicator-init lines ("comm ... nRanks N ...") on stderr so
-        # a multi-GPU run's log shows the communicator size (not the JSON line)
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     scaling = args.scaling if world > 1 else "weak"
