@@ -784,19 +784,26 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
       // late steps: the trailing update (~2 m (n_i - b) b flops) is shorter than
       // the latency-bound panel QR, SMs idle there -- one more Jacobi sweep
       if (2.0 * double(m) * double(ni - b) * double(b) < 0.4e-3 * 30e12) svd_sweep_here();
-      if (la_next) {  // G' = [0_b; G_{i+1}] next to W_u (Philox draw of step i+1)
-        gaussian_fill(hp, w.WG + size_t(b) * m + b, m, mi - b, bw_next, seed, uint32_t(i), 0u);
-        set_zero(hp, b, bw_next, w.WG + size_t(b) * m, m);
+      // G' = [0_b; G_{i+1}] next to W_u (Philox draw of step i+1), on a
+      // helper stream beside the panel QR (only G'' below needs it)
+      cudaEvent_t gdraw = overlap_event(14);
+      if (la_next) {
+        cudaStream_t gs = side_stream(3);
+        RUTV_CK(cudaStreamWaitEvent(gs, fork2, 0));
+        gaussian_fill(gs, w.WG + size_t(b) * m + b, m, mi - b, bw_next, seed, uint32_t(i), 0u);
+        set_zero(gs, b, bw_next, w.WG + size_t(b) * m, m);
+        RUTV_CK(cudaEventRecord(gdraw, gs));
       }
-      copy_matrix(hp, mi, b, X, m, Wu, ldwu);
       double* Tu = w.Tu + size_t(si) * b * b;
       double* R11 = w.Rall + size_t(si) * b * b;
       QrWork qwu = w.qw;  // R11 enters T: CholeskyQR2 only while R is backward stable
       qwu.orth_tol = kRFactorOrthTol;
+      qwu.in = X;         // the panel is read in place; W_u goes to Wu
+      qwu.ldin = m;
       check_qr(panel_qr(hp, mi, b, Wu, ldwu, R11, b, w.tau, Tu, b, qwu));
       // T(I2,J2) = R11 (replaced by D after the batched SVD), T(I3,J2) = 0
-      copy_matrix(hp, b, b, R11, b, X, m);
-      set_zero(hp, mi - b, b, X + b, m);
+      put_r_panel(hp, mi, b, R11, b, X, m);
+      if (la_next) RUTV_CK(cudaStreamWaitEvent(hp, gdraw, 0));
       if (la_next) {
         // G'' = U G' = G' - W_u (T_u (W_u^T G')), so that C^T G'' = (U^T C)^T G'
         // = X'^T G_{i+1}; and WT = W_u T_u^T for the left update C -= WT (C^T W_u)^T.

@@ -70,6 +70,8 @@ void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd)
 // D (n x m) = S^T for an m x n S
 void transpose_matrix(cudaStream_t st, int64_t m, int64_t n, const double* S, int64_t lds, double* D, int64_t ldd);
 void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd);
+// D(0:b, 0:b) = R (b x b), D(b:m, 0:b) = 0 -- the panel column block after its QR
+void put_r_panel(cudaStream_t st, int64_t m, int64_t b, const double* R, int64_t ldr, double* D, int64_t ldd);
 // Copy S -> D (may alias when equal), accumulate sum of squares and a
 // non-finite flag.  out2[0] = ||S||_F^2 (deterministic two-pass), flag[0] != 0 if any
 // entry is NaN/Inf.  ``scratch`` needs 4096 doubles.
@@ -133,6 +135,10 @@ struct QrWork {
   int* dev_flags = nullptr;
   int* flag_count = nullptr;  // host counter (slots used)
   int flag_cap = 0;
+  // panel_qr only: when set, the panel is read from `in` (ld ldin) instead of
+  // V (V is then output only; the Householder fallback copies in -> V first)
+  const double* in = nullptr;
+  int64_t ldin = 0;
 };
 // writes flag = (stats[0] != 0 || stats[2] > kappa_max * stats[1]) (CholeskyQR re-orthonormalization test)
 void reortho_flag(cudaStream_t st, const double* stats, double kappa_max, int* flag);

@@ -24,6 +24,15 @@ __global__ void scale_k(int64_t m, int64_t n, double beta, double* C, int64_t ld
       C[i + j * ldc] = beta == 0.0 ? 0.0 : beta * C[i + j * ldc];
 }
 
+// D(r, c) = r < b ? R(r, c) : 0, r < m, c < b
+__global__ void put_r_panel_k(int64_t m, int64_t b, const double* __restrict__ R, int64_t ldr, double* __restrict__ D,
+                              int64_t ldd) {
+  pdl_begin();
+  for (int64_t c = blockIdx.y; c < b; c += gridDim.y)
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m; r += int64_t(gridDim.x) * blockDim.x)
+      D[r + c * ldd] = r < b ? R[r + c * ldr] : 0.0;
+}
+
 __global__ void copy_k(int64_t m, int64_t n, const double* __restrict__ S, int64_t lds, double* __restrict__ D,
                        int64_t ldd) {
   pdl_begin();
@@ -155,6 +164,12 @@ void set_identity(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd)
 void set_zero(cudaStream_t st, int64_t m, int64_t n, double* D, int64_t ldd) {
   if (m <= 0 || n <= 0) return;
   { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(ident_k, dim3(grid2(m, n)), dim3(TB), 0, st, m, n, D, ldd, 0.0); }
+  RUTV_LAUNCH_CK();
+}
+
+void put_r_panel(cudaStream_t st, int64_t m, int64_t b, const double* R, int64_t ldr, double* D, int64_t ldd) {
+  if (m <= 0 || b <= 0) return;
+  { ProfScope _p(st, K_MISC, 0.0); count_launch(K_MISC); launch_k(put_r_panel_k, dim3(grid2(m, b)), dim3(TB), 0, st, m, b, R, ldr, D, ldd); }
   RUTV_LAUNCH_CK();
 }
 

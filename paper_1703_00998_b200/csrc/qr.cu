@@ -595,13 +595,15 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
              double* Tw, int64_t ldt, const QrWork& w) {
   if (b <= 0) return OK;
   if (m < b) return ERR_UNSUPPORTED;
+  const double* A0 = w.in ? w.in : V;  // the panel (read by the first CholeskyQR pass only)
+  const int64_t lda0 = w.in ? w.ldin : ldv;
   if (cholqr_ok(w, m, b)) {
     GemmRole role(C_GEMM_QR);
     SmallWork sw = carve_small(w.small, b);
     const int bp = sw.bp;
-    dgemm(st, true, false, b, b, m, 1.0, V, ldv, V, ldv, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);  // G1 (upper)
+    dgemm(st, true, false, b, b, m, 1.0, A0, lda0, A0, lda0, 0.0, sw.W1, bp, w.part, w.part_elems, 0, false, true);  // G1 (upper)
     small_chol_inv(st, b, sw);                                                                          // R1, R1^-1
-    dgemm(st, false, false, m, b, b, 1.0, V, ldv, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems, 0, true);  // Q1
+    dgemm(st, false, false, m, b, b, 1.0, A0, lda0, sw.R1i, bp, 0.0, w.q1, m, w.part, w.part_elems, 0, true);  // Q1
     dgemm(st, true, false, b, b, m, 1.0, w.q1, m, w.q1, m, 0.0, sw.W2, bp, w.part, w.part_elems, 0, false, true);  // G2
     const bool optimistic = w.dev_flags && w.flag_count && *w.flag_count < w.flag_cap;
     if (optimistic) sw.flag = w.dev_flags + (*w.flag_count)++;
@@ -619,6 +621,7 @@ int panel_qr(cudaStream_t st, int64_t m, int64_t b, double* V, int64_t ldv, doub
     if (ok) return OK;
     if (w.fallbacks) ++*w.fallbacks;
   }
+  if (w.in) copy_matrix(st, m, b, w.in, w.ldin, V, ldv);  // the Householder path works in place
   return panel_qr_hh(st, m, b, V, ldv, R, ldr, tau, Tw, ldt, w);
 }
 
