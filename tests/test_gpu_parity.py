@@ -79,6 +79,27 @@ def test_dgemm_tma_path():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("env", [
+    {"RANDUTV_GEMM_CLUSTER": "0"},                              # HBM partials + splitk_reduce
+    {"RANDUTV_GEMM_CLUSTER": "1"},                              # cluster epilogue, partial-costed plans
+    {"RANDUTV_GEMM_CLUSTER": "3"},                              # cluster epilogue on every <= 8-split grid
+    {"RANDUTV_GEMM_CLUSTER": "3", "RANDUTV_GEMM_SPLITS": "3"},  # forced split counts through the cluster
+    {"RANDUTV_GEMM_CLUSTER": "3", "RANDUTV_GEMM_SPLITS": "8"},
+    {"RANDUTV_GEMM_CLUSTER": "3", "RANDUTV_GEMM_SPLITS": "8", "RANDUTV_GEMM_TMA": "1"},  # TMA tiles
+    {"RANDUTV_GEMM_SPLITS": "12"},                              # > 8 splits: the partial workspace
+])
+def test_dgemm_split_k_paths(env):
+    """The split-K variants (DSMEM cluster reduction, HBM partials) on the same
+    parity cases, each in a fresh process (the switches are read once)."""
+    import subprocess
+    import sys
+    import os
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "test_dgemm_vs_oracle_matmul or test_dgemm_misaligned_views"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_dgemm_misaligned_views():
     """Odd leading dimensions and odd offsets take the 8-byte load path."""
     rng = np.random.default_rng(1)
