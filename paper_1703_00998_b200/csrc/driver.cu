@@ -917,7 +917,12 @@ int factor_device(const randutv_opts& o, int64_t m, int64_t n, const double* A, 
     jacobi_svd_batched(st, 1, (int)kf, w.Rfin, kf, kf * kf, w.Dfin, w.Usfin, w.Vsfin, w.jworkf, w.sweeps + steps);
 
   // ---- the remaining folds (the last chunks)
-  for (; folded < chunks.size(); ++folded) fold_chunk(chunks[folded]);
+  for (; folded < chunks.size(); ++folded) {
+    fold_chunk(chunks[folded]);
+    // host-staged calls: this chunk's column blocks are final -- their copy back overlaps the
+    // wait for the last chunk's SVDs and its folds
+    if (on_final) on_final(b * chunks[folded].s1, st);
+  }
   if (final_block && final_fat) {
     // T(I2, J) = [diag(D) 0];  T(I1, J) <- T(I1, J) Q blockdiag(Ur, I)
     write_diag_block(st, mif, mif, w.Dfin, T + r0f + r0f * m, m);
@@ -1221,8 +1226,14 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     double* dT = stage;
     double* dU = U ? stage + size_t(m) * n : nullptr;
     double* dV = U ? dU + size_t(m) * m : nullptr;
-    RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
-                              cudaMemcpyDefault, st));
+    auto stage_in = [&]() {  // contiguous input: one linear copy
+      if (lda == m)
+        RUTV_CK(cudaMemcpyAsync(dT, A, sizeof(double) * size_t(m) * n, cudaMemcpyDefault, st));
+      else
+        RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
+                                  cudaMemcpyDefault, st));
+    };
+    stage_in();
     // T host buffer pinned: copy T's column blocks back as they become final
     // (after each in-loop fold) on a copy stream, overlapping the rest of the
     // factorization; the remainder is copied at the end.  Not when T aliases
@@ -1252,8 +1263,7 @@ int randutv_factor_ex(const randutv_opts* opts, int64_t m, int64_t n, const doub
     if (rc == kRetry) {  // the input was factored in place: stage it again
       if (cps) RUTV_CK(cudaStreamSynchronize(cps));  // in-flight copies of the discarded run
       copied = 0;
-      RUTV_CK(cudaMemcpy2DAsync(dT, sizeof(double) * m, A, sizeof(double) * lda, sizeof(double) * m, n,
-                                cudaMemcpyDefault, st));
+      stage_in();
       rc = factor_device(o, m, n, dT, m, b, q, seed, k_stop, dU, dT, dV, info, ws, wsb, false, on_final);
     }
     if (rc == RANDUTV_OK) {
