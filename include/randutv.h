@@ -107,7 +107,10 @@ typedef struct randutv_info {
  *              both be NULL; NULL selects the paper's "no orthonormal
  *              matrices" mode.
  * U, T, V must all be host or all be device memory.  Host buffers are staged
- * through device memory inside the call.  Returns after completion.
+ * through device memory inside the call (a T-only call on a page-locked T
+ * streams T's finished column blocks back while the factorization goes on).
+ * Returns after completion; on an error return the contents of U, T, V are
+ * undefined (T may be partly written), A is never modified unless T aliases it.
  */
 RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int32_t q, uint64_t seed,
                    int64_t k_stop, double* U, double* T, double* V);
