@@ -217,6 +217,27 @@ def test_graph_replay_bitwise(uv, name, scale):
     assert par["diag_ok"] and par["ek_ok"], par
 
 
+@pytest.mark.parametrize("pin", [True, False])
+def test_host_input_with_leading_dimension(pin):
+    """Host A with lda > m (staged by the 2-D copy) against the contiguous host call
+    (staged by one linear copy): the same bytes reach the device, so T is bitwise equal;
+    pinned T (streamed copy-back, also of the tail chunks) and pageable T."""
+    m, n, b, q, pad = 1100, 900, 64, 1, 7
+    A = testmat.gaussian(m, n, 77)
+    Ac = torch.from_numpy(np.ascontiguousarray(A.T))                # (n, m): column-major A, lda = m
+    Ap = torch.full((n, m + pad), float("nan"), dtype=torch.float64)  # lda = m + pad, NaN in the padding
+    Ap[:, :m] = Ac
+    T1 = torch.empty(n, m, dtype=torch.float64)
+    T2 = torch.empty(n, m, dtype=torch.float64)
+    if pin:
+        Ac, Ap, T1, T2 = Ac.pin_memory(), Ap.pin_memory(), T1.pin_memory(), T2.pin_memory()
+    assert P.factor_raw(m, n, Ac.data_ptr(), m, b, q, 5, 0, None, T1.data_ptr(), None) == 0
+    assert P.factor_raw(m, n, Ap.data_ptr(), m + pad, b, q, 5, 0, None, T2.data_ptr(), None) == 0
+    assert torch.equal(T1, T2)
+    assert bool(torch.isfinite(T1).all())
+    assert diag_blocks_ok(T1.t().numpy()[:n, :n], b, n)
+
+
 @pytest.mark.parametrize("m,n,b,q", [(3000, 3000, 64, 1), (2600, 2000, 128, 2)])
 def test_pinned_host_copy_back_ordering(m, n, b, q):
     """Host-staged calls copy T's finished column blocks back while the loop
